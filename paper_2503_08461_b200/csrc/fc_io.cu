@@ -1,0 +1,238 @@
+// fc_io.cu -- payload movement kernels: the K8 synthetic KV generator, dense
+// <-> paged token copies (prefill ingest, P.Store of PAPER.md:246), and the
+// standalone K7 compress_tensor (reference kv.py:211-239).
+#include <cstring>
+
+#include "fc_internal.cuh"
+
+namespace fc {
+
+// ---------------------------------------------------------------------------
+// K8: counter-based generator, bit-identical to oracle/synth.py
+// ---------------------------------------------------------------------------
+constexpr int kMaxSynth = 256;
+struct SynthBatch {
+  int32_t n;
+  int32_t slot[kMaxSynth];
+  int32_t T[kMaxSynth];
+  uint64_t key[kMaxSynth];
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t splitmix(uint64_t z) { return mix64(z + 0x9E3779B97F4A7C15ull); }
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    synth_fill_kernel(char* __restrict__ arena, const int32_t* __restrict__ table, const Geom g,
+                      const __grid_constant__ SynthBatch b, uint64_t seed, int dist) {
+  constexpr int kEPV = 16 / (int)sizeof(T);
+  const int r = blockIdx.y;
+  const int T_len = b.T[r];
+  const int vpr = (int)(g.row_bytes / 16);
+  const int64_t total = (int64_t)g.L * 2 * g.H * T_len * vpr;
+  const uint64_t req = splitmix(seed ^ splitmix(b.key[r]));
+  const int32_t* row_tab = table + (int64_t)b.slot[r] * g.max_bpr;
+  const float inv_std = 0x1.bb67aep-16f;  // f32(1 / 37837.227), oracle/synth.py INV_STD
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int vec = (int)(v % vpr);
+    int64_t rest = v / vpr;
+    const int t = (int)(rest % T_len);
+    rest /= T_len;
+    const int h = (int)(rest % g.H);
+    rest /= g.H;
+    const int kv = (int)(rest % 2);
+    const int l = (int)(rest / 2);
+    const uint64_t head = splitmix(req ^ (((uint64_t)l << 24) | ((uint64_t)kv << 23) | (uint64_t)h));
+    const uint64_t row = splitmix(head ^ (uint64_t)t);
+    float scale = 1.0f;
+    if (dist == FC_SYNTH_SCALED) {
+      const float a = __fmul_rn(__uint2float_rn((uint32_t)(row >> 40)), 0x1p-24f);
+      scale = __fadd_rn(0.5f, __fmul_rn(a, 1.5f));
+    }
+    T out[kEPV];
+#pragma unroll
+    for (int e = 0; e < kEPV; ++e) {
+      const uint64_t d1 = (uint64_t)(vec * kEPV + e) + 1ull;
+      const uint64_t el = mix64(row + d1 * 0x9E3779B97F4A7C15ull);
+      const int64_t s = (int64_t)(el & 0xFFFF) + (int64_t)((el >> 16) & 0xFFFF) +
+                        (int64_t)((el >> 32) & 0xFFFF) + (int64_t)(el >> 48);
+      float x = __fmul_rn(__int2float_rn((int)(s - 131070)), inv_std);
+      if (dist == FC_SYNTH_SCALED) x = __fmul_rn(x, scale);
+      out[e] = Elem<T>::from_f(x);
+    }
+    char* dst = arena + g.seg_base(l, kv, h) + (int64_t)row_tab[t / g.bs] * g.block_stride +
+                (int64_t)(t % g.bs) * g.row_bytes + vec * 16;
+    st_stream(dst, *reinterpret_cast<uint4*>(out));
+  }
+}
+
+fc_status launch_synth(const Geom& g, int dtype, char* arena, const int32_t* table, int n,
+                       const int32_t* slots, const int32_t* tokens, const uint64_t* keys,
+                       uint64_t seed, int dist, cudaStream_t stream) {
+  for (int c = 0; c < n; c += kMaxSynth) {
+    SynthBatch b;
+    memset(&b, 0, sizeof(b));
+    b.n = n - c < kMaxSynth ? n - c : kMaxSynth;
+    int64_t max_vecs = 0;
+    for (int i = 0; i < b.n; ++i) {
+      b.slot[i] = slots[c + i];
+      b.T[i] = tokens[c + i];
+      b.key[i] = keys[c + i];
+      const int64_t vv = (int64_t)g.L * 2 * g.H * b.T[i] * (g.row_bytes / 16);
+      max_vecs = vv > max_vecs ? vv : max_vecs;
+    }
+    int64_t gx = (max_vecs + 255) / 256;
+    const int64_t cap = (148LL * 8 * 4 + b.n - 1) / b.n;
+    if (gx > cap) gx = cap;
+    if (gx < 1) gx = 1;
+    dim3 grid((unsigned)gx, (unsigned)b.n);
+    switch (dtype) {
+      case FC_F16: synth_fill_kernel<__half><<<grid, 256, 0, stream>>>(arena, table, g, b, seed, dist); break;
+      case FC_BF16: synth_fill_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>(arena, table, g, b, seed, dist); break;
+      case FC_F32: synth_fill_kernel<float><<<grid, 256, 0, stream>>>(arena, table, g, b, seed, dist); break;
+      default: return set_error(FC_ERR_UNSUPPORTED, "synth fill dtype");
+    }
+    note_launch();
+    fc_status st = cuda_check(cudaGetLastError(), "synth_fill_kernel");
+    if (st != FC_OK) return st;
+  }
+  return FC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// dense [L][2][H][n][D] <-> paged blocks
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    store_tokens_kernel(char* __restrict__ arena, const int32_t* __restrict__ row_tab, const Geom g,
+                        int64_t tok_begin, int64_t n_tok, char* __restrict__ dense, int to_blocks) {
+  const int vpr = (int)(g.row_bytes / 16);
+  const int64_t total = (int64_t)g.L * 2 * g.H * n_tok * vpr;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int vec = (int)(v % vpr);
+    int64_t rest = v / vpr;
+    const int64_t i = rest % n_tok;
+    rest /= n_tok;
+    const int h = (int)(rest % g.H);
+    rest /= g.H;
+    const int kv = (int)(rest % 2);
+    const int l = (int)(rest / 2);
+    const int64_t t = tok_begin + i;
+    char* blk = arena + g.seg_base(l, kv, h) + (int64_t)row_tab[t / g.bs] * g.block_stride +
+                (t % g.bs) * g.row_bytes + vec * 16;
+    char* dn = dense + v * 16;
+    if (to_blocks)
+      st_stream(blk, ld_stream(dn));
+    else
+      st_stream(dn, ld_stream(blk));
+  }
+}
+
+fc_status launch_store(const Geom& g, char* arena, const int32_t* table_row, int64_t tok_begin,
+                       int64_t n_tok, const void* src, bool to_blocks, cudaStream_t stream) {
+  if (((uintptr_t)src) % 16) return set_error(FC_ERR_INVALID_ARG, "dense buffer must be 16-byte aligned");
+  const int64_t total = (int64_t)g.L * 2 * g.H * n_tok * (g.row_bytes / 16);
+  int64_t grid = (total + 255) / 256;
+  if (grid > 148 * 16) grid = 148 * 16;
+  store_tokens_kernel<<<(unsigned)grid, 256, 0, stream>>>(arena, table_row, g, tok_begin, n_tok,
+                                                          (char*)src, to_blocks ? 1 : 0);
+  note_launch();
+  return cuda_check(cudaGetLastError(), "store_tokens_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// K7 standalone: compress_tensor on a dense (n, d) matrix
+// ---------------------------------------------------------------------------
+template <typename X> struct Acc { using type = float; };
+template <> struct Acc<double> { using type = double; };
+template <typename X>
+__device__ __forceinline__ typename Acc<X>::type to_acc(X x) {
+  return (typename Acc<X>::type)Elem<X>::to_f(x);
+}
+
+// numpy pairwise_sum of a contiguous run (umath loops_utils), for the (m, 1) case.
+template <typename A>
+__device__ A pairwise_sum(const A* a, int n) {
+  if (n < 8) {
+    A r = (A)0;
+    for (int i = 0; i < n; ++i) r = r + a[i];
+    return r;
+  }
+  if (n <= 128) {
+    A r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] = r[j] + a[i + j];
+    A res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res = res + a[i];
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return pairwise_sum<A>(a, n2) + pairwise_sum<A>(a + n2, n - n2);
+}
+
+template <typename X>
+__global__ void __launch_bounds__(256)
+    compress_tensor_kernel(const X* __restrict__ src, int64_t n, int64_t d, PressParams pp,
+                           void* __restrict__ dst) {
+  using A = typename Acc<X>::type;
+  const int64_t k = pp.factor;
+  const int64_t rows = (n + k - 1) / k;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < rows * d;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = o / d, c = o % d;
+    const int64_t first = r * k;
+    const int m = (int)((n - first) < k ? (n - first) : k);
+    if (pp.kind == FC_PRESS_MEANPOOL) {
+      A s;
+      if (d == 1 && (sizeof(X) == 4 || sizeof(X) == 8) && Elem<X>::kDtype != FC_BF16) {
+        s = pairwise_sum<A>(reinterpret_cast<const A*>(src) + first, m);
+      } else {
+        s = to_acc<X>(src[first * d + c]);
+        for (int i = 1; i < m; ++i) s = s + to_acc<X>(src[(first + i) * d + c]);
+      }
+      const A mean = s / (A)m;
+      reinterpret_cast<X*>(dst)[o] = Elem<X>::from_f(mean);
+    } else {
+      const double* w = pp.w_table + ((m == k) ? 0 : k);
+      double s = 0.0;
+      for (int i = 0; i < m; ++i) s = fma(w[i], (double)to_acc<X>(src[(first + i) * d + c]), s);
+      reinterpret_cast<double*>(dst)[o] = s;
+    }
+  }
+}
+
+fc_status launch_compress_tensor(const void* src, int64_t n, int64_t d, int dtype,
+                                 const PressParams& pp, void* dst, cudaStream_t stream) {
+  const int64_t rows = (n + pp.factor - 1) / pp.factor;
+  int64_t grid = (rows * d + 255) / 256;
+  if (grid > 148 * 16) grid = 148 * 16;
+  if (grid < 1) grid = 1;
+  switch (dtype) {
+    case FC_F16:
+      compress_tensor_kernel<__half><<<(unsigned)grid, 256, 0, stream>>>((const __half*)src, n, d, pp, dst);
+      break;
+    case FC_BF16:
+      compress_tensor_kernel<__nv_bfloat16><<<(unsigned)grid, 256, 0, stream>>>((const __nv_bfloat16*)src, n, d, pp, dst);
+      break;
+    case FC_F32:
+      compress_tensor_kernel<float><<<(unsigned)grid, 256, 0, stream>>>((const float*)src, n, d, pp, dst);
+      break;
+    case FC_F64:
+      compress_tensor_kernel<double><<<(unsigned)grid, 256, 0, stream>>>((const double*)src, n, d, pp, dst);
+      break;
+    default:
+      return set_error(FC_ERR_UNSUPPORTED, "compress_tensor dtype");
+  }
+  note_launch();
+  return cuda_check(cudaGetLastError(), "compress_tensor_kernel");
+}
+
+}  // namespace fc
