@@ -1,0 +1,441 @@
+#!/usr/bin/env python
+"""Benchmark of the batched KV-cache compression stage (FastCache hot path) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One *step* = one ``KVCachePool.compress_batch`` over one synthetic batch whose
+raw KV is already resident in the paged pool (Knorm / SnapKV / EA scoring +
+top-k + in-place compaction + tail-block free). Between steps the batch is
+released, re-allocated and re-filled by the K8 generator (untimed; the 18 GB
+refill also flushes L2 -- inputs are larger than L2 anyway). Step time is
+measured with CUDA events on the launch stream and summed over K steps,
+bracketed by barrier + synchronize, max over ranks.
+
+``e2e`` is the same metric through the public API with HOST buffers: every
+step copies the batch's raw KV from pinned host memory into the pool
+(H2D + ingest kernel), compresses, and reads the kept indices back (D2H).
+
+``--impl reference`` times the CPU reference arm (the oracle port of the same
+pass, oracle/cpu_pipeline.py) on the host cores, rank 0 only.
+
+Multi-GPU (torchrun): requests are sharded across ranks -- every rank
+compresses its own independent batch (weak scaling); no collective on the
+data path, NCCL only for the barrier / max-over-ranks timing.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (description, L, H, D, dtype, press, factor, n_req, lengths fn)
+    "c1": "tiny synthetic KV (4 layers, 8 heads, head_dim 64, batch 4, seq 512) Knorm 50%, fp32",
+    "c2": "LLaVA-1.5-7B-shaped KV (32 layers, 32 heads, d=128, 576 image + 512 text tokens) "
+          "batch 32, Knorm 50%, fp16",
+    "c3": "LLaVA-1.5-7B-shaped KV batch 64, SnapKV (window 32, pool 7) at 25% keep, "
+          "variable-length requests (576 img + text U[64,960])",
+    "c4w": "ExpectedAttention at 25% keep, 64 mixed-length requests (1k-8k tokens; one admission "
+           "wave of config 4)",
+}
+
+
+def workload(name: str):
+    import numpy as np
+
+    from paper_2503_08461_b200 import CompressorSpec, ModelConfig, PressKind, split_modalities
+
+    if name == "c1":
+        cfg = ModelConfig("tiny", 4, 8, 64, 4)
+        specs = [split_modalities(0, 512)] * 4
+        return cfg, "float32", specs, CompressorSpec(factor=2, press=PressKind.KNORM)
+    if name == "c2":
+        cfg = ModelConfig("llava-7b", 32, 32, 128, 2)
+        specs = [split_modalities(576, 512)] * 32
+        return cfg, "float16", specs, CompressorSpec(factor=2, press=PressKind.KNORM)
+    if name == "c3":
+        cfg = ModelConfig("llava-7b", 32, 32, 128, 2)
+        txt = np.random.default_rng(0).integers(64, 961, 64)
+        specs = [split_modalities(576, int(t)) for t in txt]
+        return cfg, "float16", specs, CompressorSpec(factor=4, press=PressKind.SNAPKV, window=32,
+                                                      pool_kernel=7)
+    if name == "c4w":
+        cfg = ModelConfig("llava-7b", 32, 32, 128, 2)
+        lens = np.random.default_rng(0).integers(1024, 8193, 256)[:64]
+        specs = [split_modalities(576, int(t) - 576) for t in lens]
+        return cfg, "float16", specs, CompressorSpec(factor=4, press=PressKind.EXPECTED_ATTENTION,
+                                                      n_sink=4)
+    raise SystemExit(f"unknown config {name}")
+
+
+def alg_bytes(cfg, specs, comp) -> int:
+    """SURVEY.md §8(d) algorithmic HBM bytes of one batch (R raw, C kept)."""
+    from paper_2503_08461_b200 import PressKind, compressed_spec, kv_bytes
+
+    raw = sum(kv_bytes(cfg, s.total_tokens) for s in specs)
+    kept = sum(kv_bytes(cfg, compressed_spec(s, comp).total_tokens) for s in specs)
+    lhq = cfg.num_layers * cfg.num_kv_heads
+    if comp.press is PressKind.KNORM:
+        return raw // 2 + 2 * kept
+    if comp.press is PressKind.SNAPKV:
+        return raw // 2 + 2 * kept + len(specs) * lhq * comp.window * cfg.head_dim * cfg.bytes_per_element
+    if comp.press is PressKind.EXPECTED_ATTENTION:
+        return raw + 2 * kept + len(specs) * lhq * (cfg.head_dim + cfg.head_dim ** 2) * 4
+    return raw + kept
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
+
+    def __init__(self, index: int, period: float = 0.05):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thr = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self._nv = None
+            return self
+        self._thr = threading.Thread(target=self._run, daemon=True)
+        self._thr.start()
+        return self
+
+    def _run(self):
+        nv = self._nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                util = nv.nvmlDeviceGetUtilizationRates(self._h).gpu
+                mhz = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                if util > 0:
+                    self.samples.append(mhz)
+                    for k, bit in names.items():
+                        if mask & bit:
+                            self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thr is not None:
+            self._thr.join()
+        return False
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def press_inputs(comp, cfg, n, device, torch, seed):
+    from paper_2503_08461_b200 import PressKind
+
+    gen = torch.Generator(device=device).manual_seed(seed)
+    if comp.press is PressKind.SNAPKV:
+        q = torch.randn((n, cfg.num_layers, cfg.num_kv_heads, comp.window, cfg.head_dim),
+                        generator=gen, device=device, dtype=torch.float32).half()
+        return {"q_window": q}
+    if comp.press is PressKind.EXPECTED_ATTENTION:
+        d = cfg.head_dim
+        mu = torch.randn((n, cfg.num_layers, cfg.num_kv_heads, d), generator=gen, device=device) / d ** 0.5
+        a = torch.randn((cfg.num_kv_heads, d, d), generator=gen, device=device)
+        cov1 = a @ a.transpose(-1, -2) / d
+        cov = cov1.expand(n, cfg.num_layers, -1, -1, -1).contiguous()
+        return {"mean_q": mu.contiguous(), "cov_q": cov}
+    return {}
+
+
+def traffic_from_profile(config: str):
+    path = os.path.join(ROOT, "profiles", f"ncu_{config}.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2503_08461_b200 import KVCachePool, _native, kv_bytes
+
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    cfg, dtype, specs, comp = workload(args.config)
+    n = len(specs)
+    raw_tokens = sum(s.total_tokens for s in specs)
+    cap = sum(kv_bytes(cfg, s.total_tokens) for s in specs)
+    pool = KVCachePool(cfg, cap, device=device, kv_dtype=dtype, max_handles=max(64, 2 * n),
+                       max_tokens_per_handle=max(s.total_tokens for s in specs) + 64,
+                       num_q_heads=cfg.num_kv_heads)
+    pool.set_profiling(True)
+    ins = press_inputs(comp, cfg, n, device, torch, seed=1234 + rank)
+    rids = [rank * 1_000_000 + i for i in range(n)]
+    stream = torch.cuda.current_stream(device)
+
+    def fill():
+        hs = pool.allocate_batch(rids, specs, 0.0)
+        pool.synth_fill(hs, seed=17)
+        return hs
+
+    press_ms, step_ms, launches, press_launches = [], [], 0, 0
+    for i in range(args.warmup):
+        hs = fill()
+        pool.compress_batch(hs, comp, 1.0, **ins)
+        pool.release_batch(hs, 2.0)
+    torch.cuda.synchronize(device)
+    if world > 1:
+        torch.distributed.barrier()
+    with ClockSampler(device.index) as clocks:
+        for i in range(args.steps):
+            hs = fill()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            pool.compress_batch(hs, comp, 1.0, **ins)
+            ev1.record(stream)
+            prof = pool.last_profile()
+            ev1.synchronize()
+            step_ms.append(ev0.elapsed_time(ev1))
+            press_ms.append(prof["press_ms"])
+            launches += prof["total_launches"]
+            press_launches += prof["press_launches"]
+            pool.release_batch(hs, 2.0)
+        torch.cuda.synchronize(device)
+    if world > 1:
+        torch.distributed.barrier()
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = raw_tokens * world * args.steps / (max_ms / 1e3)
+    abytes = alg_bytes(cfg, specs, comp)
+    peak, peak_kind = measured_peak()
+    press_avg = statistics.mean(press_ms)
+    achieved = abytes / (press_avg / 1e3) / 1e9
+    result = {
+        "metric": "compressed KV tokens/s",
+        "value": value,
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": max_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": {"float16": "f16", "bfloat16": "bf16", "float32": "f32"}[dtype],
+        "data": "synthetic (deterministic counter-based KV generator, oracle/synth.py)",
+        "config": {
+            "workload": f"{args.config}: {CONFIGS[args.config]}",
+            "press": comp.press.value, "factor": comp.factor, "requests_per_gpu": n,
+            "raw_tokens_per_gpu": raw_tokens,
+            "parallelism": f"request-sharded x{world} (independent batches, no data-path collective)",
+            "l2": "inputs larger than L2 (raw KV %.1f GB/GPU) and re-filled between steps"
+                  % (cap / 1e9),
+            "timing": "CUDA events on the launch stream around compress_batch, summed over steps",
+        },
+        "hbm_gbs": abytes * world * args.steps / (max_ms / 1e3) / 1e9 / world,
+        "roofline": {
+            "bound": "hbm", "kernel": "press_kernel (score + top-k + in-place compaction)",
+            "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic_from_profile(args.config),
+            "alg_bytes_per_step": abytes,
+            "press_launches_per_step": press_launches / args.steps,
+            "press_ms": press_avg,
+        },
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if args.e2e_steps > 0:
+        result["e2e"] = run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world)
+    return result
+
+
+def run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world):
+    """Same metric through the public API with host buffers: H2D raw KV + compress + D2H kept."""
+    import torch
+
+    stream = torch.cuda.current_stream(device)
+    n = len(specs)
+    shapes = [(cfg.num_layers, 2, cfg.num_kv_heads, s.total_tokens, cfg.head_dim) for s in specs]
+    tdt = getattr(torch, dtype)
+    hs = pool.allocate_batch(rids, specs, 0.0)
+    pool.synth_fill(hs, seed=17)
+    host = []
+    for h, shp in zip(hs, shapes):
+        buf = torch.empty(shp, dtype=tdt, pin_memory=True)
+        buf.copy_(pool.load_tokens(h))
+        host.append(buf)
+    pool.release_batch(hs, 0.0)
+    staging = [torch.empty(shp, dtype=tdt, device=device) for shp in shapes]
+    h2d = sum(b.numel() * b.element_size() for b in host)
+    kept_host = None
+    times, d2h = [], 0
+    for step in range(args.warmup + args.e2e_steps):
+        hs = pool.allocate_batch(rids, specs, 0.0)
+        torch.cuda.synchronize(device)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for h, st, hb in zip(hs, staging, host):
+            st.copy_(hb, non_blocking=True)
+            pool.store_tokens(h, st)
+        res = pool.compress_batch(hs, comp, 1.0, return_indices=True, **ins)
+        flat = torch.cat([k.reshape(-1) for k in res.kept_idx])
+        if kept_host is None:
+            kept_host = torch.empty(flat.shape, dtype=flat.dtype, pin_memory=True)
+        kept_host.copy_(flat, non_blocking=True)
+        ev1.record(stream)
+        ev1.synchronize()
+        if step >= args.warmup:
+            times.append(ev0.elapsed_time(ev1))
+            d2h = kept_host.numel() * kept_host.element_size()
+        pool.release_batch(hs, 2.0)
+    t = torch.tensor([sum(times)], dtype=torch.float64, device=device)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    tokens = sum(s.total_tokens for s in specs) * world * len(times)
+    return {"value": tokens / (float(t.item()) / 1e3), "unit": "tokens/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": float(t.item()) / len(times),
+            "path": "pinned host KV -> H2D -> store_tokens (ingest kernel) -> compress_batch -> "
+                    "kept indices D2H"}
+
+
+def cpu_reference(args, cfg, dtype, specs, comp, reps: int | None = None):
+    """The oracle port of the same pass, timed on the host cores (bounded sample)."""
+    import numpy as np
+
+    from oracle import cpu_pipeline
+    from paper_2503_08461_b200 import PressKind
+
+    workers = len(os.sched_getaffinity(0))
+    s0 = specs[0]
+    segs = [seg.token_count for seg in s0.segments]
+    rng = np.random.default_rng(0)
+    np_dt = {"float16": np.float16, "float32": np.float32, "bfloat16": np.float32}[dtype]
+    kv = rng.standard_normal((cfg.num_layers, 2, cfg.num_kv_heads, s0.total_tokens, cfg.head_dim),
+                             dtype=np.float32).astype(np_dt)
+    if comp.press is not PressKind.KNORM:
+        note = " (Knorm port used as the CPU reference pass; the SnapKV/EA ports are slower)"
+    else:
+        note = ""
+    n_req = reps or workers
+    r = cpu_pipeline.time_knorm_requests(kv, segs, comp.factor, n_req, workers,
+                                         cfg.bytes_per_element)
+    sample = (f"{n_req} requests x {cfg.num_layers} layers x {cfg.num_kv_heads} heads x "
+              f"{s0.total_tokens} tokens (oracle/cpu_pipeline.knorm_compress_request: Knorm scores, "
+              f"stable top-k, ascending K/V gather), one request per process, KV drawn once and "
+              f"shared{note}")
+    return {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["workers"], "kind": "port",
+            "sample": sample, "seconds": r["seconds"],
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def run_reference(args):
+    cfg, dtype, specs, comp = workload(args.config)
+    times = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        last = cpu_reference(args, cfg, dtype, specs, comp)
+        if i >= args.warmup:
+            times.append(last["seconds"])
+    tokens = last["value"] * last["seconds"]
+    value = tokens * len(times) / sum(times)
+    cb = dict(last)
+    cb["value"] = value
+    return {
+        "metric": "compressed KV tokens/s", "value": value, "unit": "tokens/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16" if dtype == "float16" else dtype,
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{args.config}: {CONFIGS[args.config]}",
+                   "note": "CPU reference arm: the reference has no tensor-level press "
+                           "(SURVEY.md §0); this is the oracle port of the same pass"},
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    import torch
+
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    result = run_ours(args, rank, world, local_rank)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cfg, dtype, specs, comp = workload(args.config)
+        result["cpu_baseline"] = cpu_reference(args, cfg, dtype, specs, comp)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

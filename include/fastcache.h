@@ -187,6 +187,19 @@ FC_API fc_status fc_pool_release_batch(fc_pool* pool, int32_t n, const int64_t* 
 FC_API fc_status fc_pool_get_stats(fc_pool* pool, fc_pool_stats* out);
 FC_API fc_status fc_pool_synchronize(fc_pool* pool);
 
+/* Kernel timing (CUDA events recorded on the launch stream around the press
+ * kernels and the tail-free step of each fc_pool_compress_batch call). */
+typedef struct fc_profile {
+  double press_ms;       /* press kernel(s): score + top-k + compaction          */
+  double free_ms;        /* tail-block push kernel                               */
+  double total_ms;       /* whole device span of the call                        */
+  int64_t press_launches;
+  int64_t total_launches;
+} fc_profile;
+FC_API fc_status fc_pool_set_profiling(fc_pool* pool, int32_t enable);
+/* Synchronising: timings of the most recent compress call. */
+FC_API fc_status fc_pool_last_profile(fc_pool* pool, fc_profile* out);
+
 /* Device pointer of a handle's block-table row and its live block count. */
 FC_API fc_status fc_pool_block_table(fc_pool* pool, int64_t handle_id, const int32_t** dev_row,
                               int32_t* n_blocks, int64_t* n_tokens);

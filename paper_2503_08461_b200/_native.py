@@ -40,6 +40,7 @@ EXPORTS = (
     "fc_pool_arena", "fc_pool_alloc_batch", "fc_pool_compress_batch", "fc_pool_append",
     "fc_pool_release_batch", "fc_pool_get_stats", "fc_pool_synchronize", "fc_pool_block_table",
     "fc_pool_store_tokens", "fc_pool_load_tokens", "fc_synth_fill", "fc_compress_tensor",
+    "fc_pool_set_profiling", "fc_pool_last_profile",
 )
 
 
@@ -87,6 +88,12 @@ class PoolStatsC(ctypes.Structure):
                 ("device_error", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
+class ProfileC(ctypes.Structure):
+    _fields_ = [("press_ms", ctypes.c_double), ("free_ms", ctypes.c_double),
+                ("total_ms", ctypes.c_double), ("press_launches", ctypes.c_int64),
+                ("total_launches", ctypes.c_int64)]
+
+
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
@@ -115,6 +122,8 @@ _SIGS = {
     "fc_pool_load_tokens": (_I32, [_P, _I64, _I64, _I64, _P, _P]),
     "fc_synth_fill": (_I32, [_P, _I32, _PI64, _PI64, _U64, _I32, _P]),
     "fc_compress_tensor": (_I32, [_P, _I64, _I64, _I32, ctypes.POINTER(PressConfigC), _P, _P]),
+    "fc_pool_set_profiling": (_I32, [_P, _I32]),
+    "fc_pool_last_profile": (_I32, [_P, ctypes.POINTER(ProfileC)]),
 }
 
 _lib = None

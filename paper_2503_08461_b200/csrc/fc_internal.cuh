@@ -30,6 +30,7 @@ constexpr int kMaxAllocBatch = 512; // requests per pop/push launch
 // Geometry of a pool, passed by value to kernels.
 struct Geom {
   int32_t L, H, D, bs;       // layers, kv heads, head dim, block size (tokens)
+  int32_t bs_shift;          // log2(bs): block size is a power of two
   int32_t bpe;               // bytes per element
   int32_t max_bpr;           // block-table row stride
   int64_t num_blocks;

@@ -132,6 +132,10 @@ struct fc_pool {
   std::vector<int32_t> free_slots;
   std::unordered_map<int64_t, int32_t> h2s;
   int64_t next_id = 0;
+  bool profiling = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, press_end, free_end, end
+  int64_t prof_press_launches = 0, prof_total_launches = 0;
+  bool prof_valid = false;
 };
 
 namespace {
@@ -251,6 +255,8 @@ fc_status fc_pool_create(const fc_model_config* cfg, uint64_t capacity_bytes,
   if (capacity_bytes < 1) return set_error(FC_ERR_INVALID_ARG, "capacity_bytes must be >= 1");
   if (opts->block_size < 1 || opts->max_handles < 1 || opts->max_blocks_per_handle < 1)
     return set_error(FC_ERR_INVALID_ARG, "block_size, max_handles, max_blocks_per_handle must be >= 1");
+  if (opts->block_size & (opts->block_size - 1))
+    return set_error(FC_ERR_UNSUPPORTED, "block_size must be a power of two");
   if (((int64_t)cfg->head_dim * cfg->bytes_per_element) % 16 != 0)
     return set_error(FC_ERR_UNSUPPORTED, "head_dim * bytes_per_element must be a multiple of 16");
 
@@ -267,6 +273,8 @@ fc_status fc_pool_create(const fc_model_config* cfg, uint64_t capacity_bytes,
   g.H = cfg->num_kv_heads;
   g.D = cfg->head_dim;
   g.bs = opts->block_size;
+  g.bs_shift = 0;
+  while ((1 << g.bs_shift) < g.bs) ++g.bs_shift;
   g.bpe = cfg->bytes_per_element;
   g.max_bpr = opts->max_blocks_per_handle;
   g.num_blocks = opts->num_blocks > 0
@@ -331,6 +339,8 @@ fc_status fc_pool_destroy(fc_pool* p) {
   cudaFree(p->d_err);
   cudaFree(p->d_wtable);
   cudaFree(p->d_ws);
+  for (auto& e : p->ev)
+    if (e) cudaEventDestroy(e);
   delete p;
   return FC_OK;
 }
@@ -460,6 +470,8 @@ fc_status fc_pool_compress_batch(fc_pool* p, int32_t n, const int64_t* handle_id
 
   DeviceGuard guard(p->device);
   fc_status st;
+  const int64_t launches0 = g_launches;
+  if (p->profiling) cudaEventRecord(p->ev[0], stream);
   // Legacy: move the raw rows aside and pop fresh destination blocks (batch order).
   if (legacy) {
     std::vector<BlockOp> ops(n);
@@ -544,6 +556,8 @@ fc_status fc_pool_compress_batch(fc_pool* p, int32_t n, const int64_t* handle_id
     if (st != FC_OK) return st;
   }
 
+  int64_t press_launches = g_launches - launches0;
+  if (p->profiling) cudaEventRecord(p->ev[1], stream);
   // Pooled: free the tail blocks in the same stream step (zero-zombie reclaim).
   if (!legacy) {
     std::vector<BlockOp> ops(n);
@@ -554,6 +568,13 @@ fc_status fc_pool_compress_batch(fc_pool* p, int32_t n, const int64_t* handle_id
     }
     st = run_block_ops(p, ops, false, false, {}, stream);
     if (st != FC_OK) return st;
+  }
+  if (p->profiling) {
+    cudaEventRecord(p->ev[2], stream);
+    cudaEventRecord(p->ev[3], stream);
+    p->prof_press_launches = press_launches;
+    p->prof_total_launches = g_launches - launches0;
+    p->prof_valid = true;
   }
 
   // Host accounting, batch order (engine.py:501-510 -> pool.py:167-192).
@@ -719,6 +740,38 @@ fc_status fc_pool_get_stats(fc_pool* p, fc_pool_stats* out) {
   out->fragmentation = used > 0 ? 1.0 - (double)live_tok / used : 0.0;
   out->device_error = st == FC_ERR_DEVICE ? 1 : 0;
   return st;
+}
+
+fc_status fc_pool_set_profiling(fc_pool* p, int32_t enable) {
+  if (!p) return set_error(FC_ERR_INVALID_ARG, "null pool");
+  DeviceGuard guard(p->device);
+  if (enable && !p->ev[0]) {
+    for (auto& e : p->ev) {
+      fc_status st = cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+      if (st != FC_OK) return st;
+    }
+  }
+  p->profiling = enable != 0;
+  p->prof_valid = false;
+  return FC_OK;
+}
+
+fc_status fc_pool_last_profile(fc_pool* p, fc_profile* out) {
+  if (!p || !out) return set_error(FC_ERR_INVALID_ARG, "null argument");
+  if (!p->prof_valid) return set_error(FC_ERR_INVALID_STATE, "no profiled compress call");
+  DeviceGuard guard(p->device);
+  fc_status st = cuda_check(cudaEventSynchronize(p->ev[3]), "cudaEventSynchronize");
+  if (st != FC_OK) return st;
+  float a = 0, b = 0, c = 0;
+  cudaEventElapsedTime(&a, p->ev[0], p->ev[1]);
+  cudaEventElapsedTime(&b, p->ev[1], p->ev[2]);
+  cudaEventElapsedTime(&c, p->ev[0], p->ev[3]);
+  out->press_ms = a;
+  out->free_ms = b;
+  out->total_ms = c;
+  out->press_launches = p->prof_press_launches;
+  out->total_launches = p->prof_total_launches;
+  return FC_OK;
 }
 
 fc_status fc_pool_block_table(fc_pool* p, int64_t handle_id, const int32_t** dev_row,

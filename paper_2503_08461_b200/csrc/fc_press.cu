@@ -151,12 +151,16 @@ struct RowCfg {
 template <typename T, int D>
 __device__ __forceinline__ void score_knorm(const char* __restrict__ seg, const Geom& g,
                                             const int32_t* s_tab, int T_len, float* sc) {
-  constexpr int kVecs = D * (int)sizeof(T) / 16;
+  constexpr int kRowBytes = D * (int)sizeof(T);
+  constexpr int kVecs = kRowBytes / 16;
   constexpr int kLPR = kVecs < 32 ? kVecs : 32;
   constexpr int kVPL = kVecs / kLPR;
   constexpr int kEPV = RowCfg<T>::kEPV;
   constexpr int kRPP = kThreads / kLPR;
   constexpr int kU = 4;
+  // For 16-bit inputs x*x is exact in fp32, so fma(x, x, acc) rounds exactly
+  // like fadd(fmul(x, x), acc) (the oracle's order) with half the instructions.
+  constexpr bool kExactSquare = sizeof(T) == 2;
   const int lr = threadIdx.x % kLPR, rp = threadIdx.x / kLPR;
   for (int t0 = 0; t0 < T_len; t0 += kRPP * kU) {
     uint4 v[kU][kVPL];
@@ -164,7 +168,8 @@ __device__ __forceinline__ void score_knorm(const char* __restrict__ seg, const 
     for (int u = 0; u < kU; ++u) {
       const int t = t0 + u * kRPP + rp;
       if (t < T_len) {
-        const char* row = seg + (int64_t)s_tab[t / g.bs] * g.block_stride + (int64_t)(t % g.bs) * g.row_bytes;
+        const char* row = seg + (int64_t)s_tab[t >> g.bs_shift] * g.block_stride +
+                          (int64_t)(t & (g.bs - 1)) * kRowBytes;
 #pragma unroll
         for (int vv = 0; vv < kVPL; ++vv) v[u][vv] = ld_stream(row + (lr + vv * kLPR) * 16);
       } else {
@@ -180,7 +185,8 @@ __device__ __forceinline__ void score_knorm(const char* __restrict__ seg, const 
         float x[kEPV];
         unpack16<T>(v[u][vv], x);
 #pragma unroll
-        for (int e = 0; e < kEPV; ++e) acc = __fadd_rn(acc, __fmul_rn(x[e], x[e]));
+        for (int e = 0; e < kEPV; ++e)
+          acc = kExactSquare ? __fmaf_rn(x[e], x[e], acc) : __fadd_rn(acc, __fmul_rn(x[e], x[e]));
       }
 #pragma unroll
       for (int off = kLPR / 2; off >= 1; off >>= 1)
@@ -206,7 +212,8 @@ __device__ __forceinline__ void scale_by_vnorm(const char* __restrict__ seg_v, c
     const int t = t0 + rp;
     float acc = 0.f;
     if (t < T_len) {
-      const char* row = seg_v + (int64_t)s_tab[t / g.bs] * g.block_stride + (int64_t)(t % g.bs) * g.row_bytes;
+      const char* row = seg_v + (int64_t)s_tab[t >> g.bs_shift] * g.block_stride +
+                        (int64_t)(t & (g.bs - 1)) * g.row_bytes;
 #pragma unroll
       for (int vv = 0; vv < kVPL; ++vv) {
         float x[kEPV];
@@ -233,7 +240,8 @@ __device__ __forceinline__ void load_rows_f32(const char* __restrict__ seg, cons
     const int t = t0 + r;
     float x[kEPV];
     if (t < T_len) {
-      const char* row = seg + (int64_t)s_tab[t / g.bs] * g.block_stride + (int64_t)(t % g.bs) * g.row_bytes;
+      const char* row = seg + (int64_t)s_tab[t >> g.bs_shift] * g.block_stride +
+                        (int64_t)(t & (g.bs - 1)) * g.row_bytes;
       unpack16<T>(ld_stream(row + vec * 16), x);
     } else {
 #pragma unroll
@@ -437,16 +445,19 @@ __device__ void score_ea(const char* __restrict__ seg, const Geom& g, const int3
 // ---------------------------------------------------------------------------
 // phase 3: in-place compaction of kept rows
 // ---------------------------------------------------------------------------
-template <int kRowBytes>
-__device__ __forceinline__ void compact_rows(char* __restrict__ seg, const Geom& g,
-                                             const int32_t* s_src, const int32_t* s_dst,
-                                             const int32_t* idx, int K, int j_start) {
-  constexpr int kVecs = kRowBytes / 16;
-  constexpr int kItems = 8;
-  constexpr int kChunk = kThreads * kItems / (2 * kVecs);
-  const int64_t kv_off = (int64_t)g.H * g.bs * kRowBytes;
-  for (int j0 = j_start; j0 < K; j0 += kChunk) {
-    uint4 buf[kItems];
+template <int kRowBytes, int kItems>
+struct Compactor {
+  static constexpr int kVecs = kRowBytes / 16;
+  static constexpr int kChunk = kThreads * kItems / (2 * kVecs);  // ranks per chunk
+  char* seg;
+  const Geom& g;
+  const int32_t* s_src;
+  const int32_t* s_dst;
+  const int32_t* idx;
+  int K;
+  int64_t kv_off;
+
+  __device__ __forceinline__ void load(int j0, uint4 (&buf)[kItems]) const {
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
       const int item = it * kThreads + threadIdx.x;
@@ -455,11 +466,12 @@ __device__ __forceinline__ void compact_rows(char* __restrict__ seg, const Geom&
       const int j = j0 + row;
       if (j < K) {
         const int src = idx[j];
-        buf[it] = ld_stream(seg + kv * kv_off + (int64_t)s_src[src / g.bs] * g.block_stride +
-                            (int64_t)(src % g.bs) * kRowBytes + vec * 16);
+        buf[it] = ld_stream(seg + kv * kv_off + (int64_t)s_src[src >> g.bs_shift] * g.block_stride +
+                            (int64_t)(src & (g.bs - 1)) * kRowBytes + vec * 16);
       }
     }
-    __syncthreads();
+  }
+  __device__ __forceinline__ void store(int j0, const uint4 (&buf)[kItems]) const {
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
       const int item = it * kThreads + threadIdx.x;
@@ -467,10 +479,42 @@ __device__ __forceinline__ void compact_rows(char* __restrict__ seg, const Geom&
       const int kv = rem / kVecs, vec = rem % kVecs;
       const int j = j0 + row;
       if (j < K)
-        st_stream(seg + kv * kv_off + (int64_t)s_dst[j / g.bs] * g.block_stride +
-                      (int64_t)(j % g.bs) * kRowBytes + vec * 16,
+        st_stream(seg + kv * kv_off + (int64_t)s_dst[j >> g.bs_shift] * g.block_stride +
+                      (int64_t)(j & (g.bs - 1)) * kRowBytes + vec * 16,
                   buf[it]);
     }
+  }
+};
+
+// Copy kept rows j <- idx[j] (K and V), chunks of kChunk ranks, software
+// pipelined: loads of chunk c+1 are in flight while chunk c is stored. Safe in
+// place because idx is ascending (idx[j] >= j): chunk c writes ranks
+// [cW, (c+1)W) while chunk c+1 only reads positions >= (c+1)W, and the barrier
+// before chunk c+1's stores orders them after every read of chunks <= c+1.
+template <int kRowBytes>
+__device__ __forceinline__ void compact_rows(char* __restrict__ seg, const Geom& g,
+                                             const int32_t* s_src, const int32_t* s_dst,
+                                             const int32_t* idx, int K, int j_start) {
+  constexpr int kItems = 4;
+  using C = Compactor<kRowBytes, kItems>;
+  const C c{seg, g, s_src, s_dst, idx, K, (int64_t)g.H * g.bs * kRowBytes};
+  if (j_start >= K) return;
+  uint4 a[kItems], b[kItems];
+  int j0 = j_start;
+  c.load(j0, a);
+  __syncthreads();
+  while (true) {
+    const int j1 = j0 + C::kChunk;
+    if (j1 < K) c.load(j1, b);
+    c.store(j0, a);
+    if (j1 >= K) break;
+    __syncthreads();
+    const int j2 = j1 + C::kChunk;
+    if (j2 < K) c.load(j2, a);
+    c.store(j1, b);
+    if (j2 >= K) break;
+    __syncthreads();
+    j0 = j2;
   }
 }
 
@@ -502,7 +546,7 @@ __host__ __device__ inline SmemPlan smem_plan(int kind, int max_T, int bs, int D
 }
 
 template <typename T, int D, int KIND>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, KIND == FC_PRESS_KNORM ? 4 : 2)
     press_kernel(char* __restrict__ arena, const int32_t* __restrict__ src_table,
                  const int32_t* __restrict__ dst_table, const Geom g,
                  const __grid_constant__ PressBatch b, const PressParams pp,
@@ -634,8 +678,8 @@ __global__ void __launch_bounds__(kThreads)
       for (int i = 0; i < m; ++i) {
         const int src = s_first + i;
         float x[kEPV];
-        unpack16<T>(ld_stream(seg + kv * kv_off + (int64_t)s_src[src / g.bs] * g.block_stride +
-                              (int64_t)(src % g.bs) * g.row_bytes + vec * 16),
+        unpack16<T>(ld_stream(seg + kv * kv_off + (int64_t)s_src[src >> g.bs_shift] * g.block_stride +
+                              (int64_t)(src & (g.bs - 1)) * g.row_bytes + vec * 16),
                     x);
         if (pp.kind == FC_PRESS_MEANPOOL) {
 #pragma unroll
@@ -664,8 +708,8 @@ __global__ void __launch_bounds__(kThreads)
       const int kv = rem / kVecs, vec = rem % kVecs;
       const int j = j0 + row;
       if (j < q.K)
-        st_stream(seg + kv * kv_off + (int64_t)s_dst[j / g.bs] * g.block_stride +
-                      (int64_t)(j % g.bs) * g.row_bytes + vec * 16,
+        st_stream(seg + kv * kv_off + (int64_t)s_dst[j >> g.bs_shift] * g.block_stride +
+                      (int64_t)(j & (g.bs - 1)) * g.row_bytes + vec * 16,
                   res[it]);
     }
     __syncthreads();

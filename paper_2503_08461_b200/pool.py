@@ -675,6 +675,19 @@ class KVCachePool:
         return BlockStats(st.num_blocks, st.free_blocks, st.used_blocks, st.block_bytes,
                           st.live_token_bytes, st.fragmentation)
 
+    def set_profiling(self, enable: bool = True) -> None:
+        """Record CUDA events around the press kernels of every compress call."""
+        nv = self._need_native()
+        nv._check(nv.lib.fc_pool_set_profiling(nv.ptr, 1 if enable else 0))
+
+    def last_profile(self) -> dict:
+        """Device timings (ms) of the most recent compress call (synchronising)."""
+        nv = self._need_native()
+        prof = nat.ProfileC()
+        nv._check(nv.lib.fc_pool_last_profile(nv.ptr, ctypes.byref(prof)))
+        return {"press_ms": prof.press_ms, "free_ms": prof.free_ms, "total_ms": prof.total_ms,
+                "press_launches": prof.press_launches, "total_launches": prof.total_launches}
+
     def synchronize(self) -> None:
         if self._native is not None:
             self._native._check(self._native.lib.fc_pool_synchronize(self._native.ptr))

@@ -51,6 +51,7 @@ def test_struct_layouts_match_ctypes():
         "fc_model_config": nat.ModelConfigC, "fc_pool_options": nat.PoolOptionsC,
         "fc_press_config": nat.PressConfigC, "fc_press_inputs": nat.PressInputsC,
         "fc_press_outputs": nat.PressOutputsC, "fc_pool_stats": nat.PoolStatsC,
+        "fc_profile": nat.ProfileC,
     }
     src = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{HEADER}"', "int main(void){"]
     for cname, cls in structs.items():
