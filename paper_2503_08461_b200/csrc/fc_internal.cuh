@@ -59,6 +59,8 @@ struct PressBatch {
   int32_t per_segment;
   int32_t in_place;      // src table == dst table
   int32_t max_T;
+  int32_t n_total;       // requests in the whole compress call (press-input rows)
+  int32_t reserved;
   PressReq req[kMaxBatch];
 };
 
@@ -150,6 +152,10 @@ fc_status launch_press(const Geom& g, int dtype, char* arena, const int32_t* src
                        int32_t* dst_table, const PressBatch& batch, const PressParams& pp,
                        const fc_press_inputs* in, const fc_press_outputs* out, float* workspace,
                        int64_t workspace_floats, int32_t* d_err, cudaStream_t stream);
+bool snapkv_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T);
+fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t* table,
+                           const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
+                           const fc_press_outputs& out, cudaStream_t stream);
 int64_t press_workspace_floats(const Geom& g, int kind, int window, int num_q_heads, int max_T);
 
 // io kernels (fc_io.cu)

@@ -527,6 +527,7 @@ fc_status fc_pool_compress_batch(fc_pool* p, int32_t n, const int64_t* handle_id
     b.n = std::min(kMaxBatch, n - c);
     b.per_segment = press->kind <= FC_PRESS_EXPECTED_ATTENTION ? 0 : 1;
     b.in_place = legacy ? 0 : 1;
+    b.n_total = n;
     for (int r = 0; r < b.n; ++r) {
       const int i = order[c + r];
       const Slot& sl = p->slots[slot[i]];

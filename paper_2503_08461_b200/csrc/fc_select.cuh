@@ -1,0 +1,201 @@
+// fc_select.cuh -- device building blocks shared by the press kernels:
+// block scans, the segmented radix top-k (select_emit) and the in-place
+// kept-row compaction (compact_rows). See fc_press.cu for the phase contract.
+#pragma once
+
+#include <climits>
+
+#include "fc_internal.cuh"
+
+namespace fc {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+struct SelectScratch {
+  uint32_t hist[256];
+  int32_t warp_tot[kWarps];
+  int32_t sel_bin;
+  int32_t sel_krem;
+  int32_t first_drop;
+  float red[kWarps * 4];
+};
+
+// Block-wide exclusive scan of a predicate (all threads must call).
+__device__ __forceinline__ int block_excl_scan(bool pred, int32_t* warp_tot, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  const int in_warp = __popc(m & ((1u << lane) - 1u));
+  if (lane == 0) warp_tot[warp] = __popc(m);
+  __syncthreads();
+  int before = 0;
+  total = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    const int c = warp_tot[w];
+    before += (w < warp) ? c : 0;
+    total += c;
+  }
+  __syncthreads();
+  return before + in_warp;
+}
+
+// Top-K of keys[0..n) by (key desc, index asc); writes idx_base + i of the kept
+// i, ascending, to out[out_base ...]. `out` may alias `keys` (write positions
+// never pass unread keys: out_base <= keys' own offset and each write index is
+// <= its source index).
+static __device__ void select_emit(const uint32_t* keys, int n, int K, int32_t* out, int out_base,
+                            int idx_base, SelectScratch& s) {
+  uint32_t tau = 0;
+  int need = 0;
+  const bool all = K >= n;
+  if (!all) {
+    uint32_t prefix = 0, mask = 0;
+    int krem = K;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += kThreads) s.hist[i] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += kThreads) {
+        const uint32_t k = keys[i];
+        if ((k & mask) == prefix) atomicAdd(&s.hist[(k >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        uint32_t c[8];
+        uint32_t local = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          c[b] = s.hist[lane * 8 + b];
+          local += c[b];
+        }
+        uint32_t incl = local;  // sum over lanes >= lane
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t y = __shfl_down_sync(0xffffffffu, incl, off);
+          if (lane + off < 32) incl += y;
+        }
+        const uint32_t above = incl - local;
+        if (above < (uint32_t)krem && (uint32_t)krem <= incl) {
+          uint32_t cum = above;
+#pragma unroll
+          for (int b = 7; b >= 0; --b) {
+            if (cum + c[b] >= (uint32_t)krem) {
+              s.sel_bin = lane * 8 + b;
+              s.sel_krem = krem - (int)cum;
+              break;
+            }
+            cum += c[b];
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= (uint32_t)s.sel_bin << shift;
+      mask |= 255u << shift;
+      krem = s.sel_krem;
+      __syncthreads();
+    }
+    tau = prefix;
+    need = krem;
+  }
+  int running = 0, running_eq = 0;
+  for (int base = 0; base < n; base += kThreads) {
+    const int i = base + threadIdx.x;
+    const bool valid = i < n;
+    const uint32_t k = valid ? keys[i] : 0u;
+    bool kept = valid;
+    if (!all) {
+      const bool eq = valid && k == tau;
+      int eq_total;
+      const int eq_pre = block_excl_scan(eq, s.warp_tot, eq_total);
+      kept = valid && (k > tau || (eq && running_eq + eq_pre < need));
+      running_eq += eq_total;
+    }
+    int tot;
+    const int pre = block_excl_scan(kept, s.warp_tot, tot);
+    if (kept) out[out_base + running + pre] = idx_base + i;
+    if (valid && !kept) atomicMin(&s.first_drop, idx_base + i);
+    running += tot;
+  }
+  __syncthreads();
+}
+
+template <typename T>
+struct RowCfg {
+  static constexpr int kEPV = 16 / sizeof(T);
+};
+
+template <int kRowBytes, int kItems>
+struct Compactor {
+  static constexpr int kVecs = kRowBytes / 16;
+  static constexpr int kChunk = kThreads * kItems / (2 * kVecs);  // ranks per chunk
+  char* seg;
+  const Geom& g;
+  const int32_t* s_src;
+  const int32_t* s_dst;
+  const int32_t* idx;
+  int K;
+  int64_t kv_off;
+
+  __device__ __forceinline__ void load(int j0, uint4 (&buf)[kItems]) const {
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int item = it * kThreads + threadIdx.x;
+      const int row = item / (2 * kVecs), rem = item % (2 * kVecs);
+      const int kv = rem / kVecs, vec = rem % kVecs;
+      const int j = j0 + row;
+      if (j < K) {
+        const int src = idx[j];
+        buf[it] = ld_stream(seg + kv * kv_off + (int64_t)s_src[src >> g.bs_shift] * g.block_stride +
+                            (int64_t)(src & (g.bs - 1)) * kRowBytes + vec * 16);
+      }
+    }
+  }
+  __device__ __forceinline__ void store(int j0, const uint4 (&buf)[kItems]) const {
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int item = it * kThreads + threadIdx.x;
+      const int row = item / (2 * kVecs), rem = item % (2 * kVecs);
+      const int kv = rem / kVecs, vec = rem % kVecs;
+      const int j = j0 + row;
+      if (j < K)
+        st_stream(seg + kv * kv_off + (int64_t)s_dst[j >> g.bs_shift] * g.block_stride +
+                      (int64_t)(j & (g.bs - 1)) * kRowBytes + vec * 16,
+                  buf[it]);
+    }
+  }
+};
+
+// Copy kept rows j <- idx[j] (K and V), chunks of kChunk ranks, software
+// pipelined: loads of chunk c+1 are in flight while chunk c is stored. Safe in
+// place because idx is ascending (idx[j] >= j): chunk c writes ranks
+// [cW, (c+1)W) while chunk c+1 only reads positions >= (c+1)W, and the barrier
+// before chunk c+1's stores orders them after every read of chunks <= c+1.
+template <int kRowBytes>
+__device__ __forceinline__ void compact_rows(char* __restrict__ seg, const Geom& g,
+                                             const int32_t* s_src, const int32_t* s_dst,
+                                             const int32_t* idx, int K, int j_start) {
+  constexpr int kItems = 4;
+  using C = Compactor<kRowBytes, kItems>;
+  const C c{seg, g, s_src, s_dst, idx, K, (int64_t)g.H * g.bs * kRowBytes};
+  if (j_start >= K) return;
+  uint4 a[kItems], b[kItems];
+  int j0 = j_start;
+  c.load(j0, a);
+  __syncthreads();
+  while (true) {
+    const int j1 = j0 + C::kChunk;
+    if (j1 < K) c.load(j1, b);
+    c.store(j0, a);
+    if (j1 >= K) break;
+    __syncthreads();
+    const int j2 = j1 + C::kChunk;
+    if (j2 < K) c.load(j2, a);
+    c.store(j1, b);
+    if (j2 >= K) break;
+    __syncthreads();
+    j0 = j2;
+  }
+}
+
+}  // namespace fc

@@ -8,6 +8,6 @@ if [ -n "$FILTER" ]; then
 fi
 python bench.py --config $CFG --steps 10 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 tail -3 gpurun_out/bench_$TAG.err; cat gpurun_out/bench_$TAG.json
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:press_kernel -s 3 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"press_kernel|snapkv_tc" -s 3 -c 1 \
   -o gpurun_out/prof_$TAG -f python bench.py --config $CFG --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_$TAG.log 2>&1
 tail -2 gpurun_out/ncu_$TAG.log

@@ -212,7 +212,9 @@ def _snap_inputs(n, L, hq, w, D, seed, device, dtype):
 
 
 @pytest.mark.parametrize("dtype,L,H,gq,D,specs,w,p", [
-    ("float16", 2, 2, 1, 128, [(576, 70), (0, 100), (40, 0)], 32, 7),
+    ("float16", 2, 2, 1, 128, [(576, 70), (0, 100), (40, 0)], 32, 7),      # tcgen05 path
+    ("bfloat16", 1, 2, 1, 128, [(576, 960), (1, 2046), (33, 0)], 32, 7),   # tcgen05, 16 tiles
+    ("float16", 2, 3, 1, 64, [(300, 17), (129, 0)], 32, 5),                # tcgen05, D=64
     ("bfloat16", 1, 2, 2, 64, [(0, 300), (100, 21)], 16, 5),
     ("float32", 1, 1, 4, 128, [(50, 50)], 8, 3),
 ])
