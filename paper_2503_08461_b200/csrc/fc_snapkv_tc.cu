@@ -51,9 +51,11 @@ __host__ __device__ inline TcSmem tc_smem_plan(int D, int w, int bs, int max_T) 
   p.off_q = p.off_stage + kTcStages * p.tile_bytes;
   p.off_tab = p.off_q + ((p.q_bytes + 1023) & ~1023);
   const int nb = (max_T + bs - 1) / bs;
-  p.off_sc = p.off_tab + ((nb * 4 + 15) & ~15);
+  // Scores (sc) and window means (s1) live in the K stage ring: they are only
+  // written after the last MMA has consumed the last stage (mma_done).
+  p.off_sc = p.off_stage;
   p.off_s1 = p.off_sc + ((max_T * 4 + 15) & ~15);
-  p.off_bar = p.off_s1 + ((max_T * 4 + 15) & ~15);
+  p.off_bar = p.off_tab + ((nb * 4 + 15) & ~15);
   p.total = p.off_bar + 16 * 8 + 1024;                        // barriers + alignment slack
   return p;
 }
