@@ -292,11 +292,12 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clocks.summary(),
     }
     if args.e2e_steps > 0:
-        result["e2e"] = run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world)
+        result["e2e"] = run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world,
+                                job_tokens)
     return result
 
 
-def run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world):
+def run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world, job_tokens):
     """Same metric through the public API with host buffers: H2D raw KV + compress + D2H kept."""
     import torch
 
@@ -338,7 +339,7 @@ def run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world):
     t = torch.tensor([sum(times)], dtype=torch.float64, device=device)
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    tokens = sum(s.total_tokens for s in specs) * world * len(times)
+    tokens = job_tokens * len(times)
     return {"value": tokens / (float(t.item()) / 1e3), "unit": "tokens/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": float(t.item()) / len(times),
