@@ -12,6 +12,20 @@ namespace fc {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
+// A set of 256 threads that cooperates on one segment: the whole CTA, or the
+// consumer warps of a warp-specialised kernel synchronising on a named barrier.
+struct CtaGroup {
+  __device__ __forceinline__ static int tid() { return threadIdx.x; }
+  __device__ __forceinline__ static void sync() { __syncthreads(); }
+};
+template <int kFirstThread, int kBarrierId>
+struct NamedGroup {
+  __device__ __forceinline__ static int tid() { return threadIdx.x - kFirstThread; }
+  __device__ __forceinline__ static void sync() {
+    asm volatile("bar.sync %0, %1;" ::"n"(kBarrierId), "n"(kThreads) : "memory");
+  }
+};
+
 struct SelectScratch {
   uint32_t hist[256];
   int32_t warp_tot[kWarps];
@@ -22,12 +36,13 @@ struct SelectScratch {
 };
 
 // Block-wide exclusive scan of a predicate (all threads must call).
+template <class G = CtaGroup>
 __device__ __forceinline__ int block_excl_scan(bool pred, int32_t* warp_tot, int& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = G::tid() >> 5;
   const unsigned m = __ballot_sync(0xffffffffu, pred);
   const int in_warp = __popc(m & ((1u << lane) - 1u));
   if (lane == 0) warp_tot[warp] = __popc(m);
-  __syncthreads();
+  G::sync();
   int before = 0;
   total = 0;
 #pragma unroll
@@ -36,7 +51,7 @@ __device__ __forceinline__ int block_excl_scan(bool pred, int32_t* warp_tot, int
     before += (w < warp) ? c : 0;
     total += c;
   }
-  __syncthreads();
+  G::sync();
   return before + in_warp;
 }
 
@@ -44,7 +59,8 @@ __device__ __forceinline__ int block_excl_scan(bool pred, int32_t* warp_tot, int
 // i, ascending, to out[out_base ...]. `out` may alias `keys` (write positions
 // never pass unread keys: out_base <= keys' own offset and each write index is
 // <= its source index).
-static __device__ void select_emit(const uint32_t* keys, int n, int K, int32_t* out, int out_base,
+template <class G = CtaGroup>
+__device__ void select_emit(const uint32_t* keys, int n, int K, int32_t* out, int out_base,
                             int idx_base, SelectScratch& s) {
   uint32_t tau = 0;
   int need = 0;
@@ -53,15 +69,15 @@ static __device__ void select_emit(const uint32_t* keys, int n, int K, int32_t* 
     uint32_t prefix = 0, mask = 0;
     int krem = K;
     for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int i = threadIdx.x; i < 256; i += kThreads) s.hist[i] = 0;
-      __syncthreads();
-      for (int i = threadIdx.x; i < n; i += kThreads) {
+      for (int i = G::tid(); i < 256; i += kThreads) s.hist[i] = 0;
+      G::sync();
+      for (int i = G::tid(); i < n; i += kThreads) {
         const uint32_t k = keys[i];
         if ((k & mask) == prefix) atomicAdd(&s.hist[(k >> shift) & 255u], 1u);
       }
-      __syncthreads();
-      if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
+      G::sync();
+      if (G::tid() < 32) {
+        const int lane = G::tid();
         uint32_t c[8];
         uint32_t local = 0;
 #pragma unroll
@@ -89,35 +105,35 @@ static __device__ void select_emit(const uint32_t* keys, int n, int K, int32_t* 
           }
         }
       }
-      __syncthreads();
+      G::sync();
       prefix |= (uint32_t)s.sel_bin << shift;
       mask |= 255u << shift;
       krem = s.sel_krem;
-      __syncthreads();
+      G::sync();
     }
     tau = prefix;
     need = krem;
   }
   int running = 0, running_eq = 0;
   for (int base = 0; base < n; base += kThreads) {
-    const int i = base + threadIdx.x;
+    const int i = base + G::tid();
     const bool valid = i < n;
     const uint32_t k = valid ? keys[i] : 0u;
     bool kept = valid;
     if (!all) {
       const bool eq = valid && k == tau;
       int eq_total;
-      const int eq_pre = block_excl_scan(eq, s.warp_tot, eq_total);
+      const int eq_pre = block_excl_scan<G>(eq, s.warp_tot, eq_total);
       kept = valid && (k > tau || (eq && running_eq + eq_pre < need));
       running_eq += eq_total;
     }
     int tot;
-    const int pre = block_excl_scan(kept, s.warp_tot, tot);
+    const int pre = block_excl_scan<G>(kept, s.warp_tot, tot);
     if (kept) out[out_base + running + pre] = idx_base + i;
     if (valid && !kept) atomicMin(&s.first_drop, idx_base + i);
     running += tot;
   }
-  __syncthreads();
+  G::sync();
 }
 
 template <typename T>
@@ -125,7 +141,7 @@ struct RowCfg {
   static constexpr int kEPV = 16 / sizeof(T);
 };
 
-template <int kRowBytes, int kItems>
+template <int kRowBytes, int kItems, class G = CtaGroup>
 struct Compactor {
   static constexpr int kVecs = kRowBytes / 16;
   static constexpr int kChunk = kThreads * kItems / (2 * kVecs);  // ranks per chunk
@@ -140,7 +156,7 @@ struct Compactor {
   __device__ __forceinline__ void load(int j0, uint4 (&buf)[kItems]) const {
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
-      const int item = it * kThreads + threadIdx.x;
+      const int item = it * kThreads + G::tid();
       const int row = item / (2 * kVecs), rem = item % (2 * kVecs);
       const int kv = rem / kVecs, vec = rem % kVecs;
       const int j = j0 + row;
@@ -154,7 +170,7 @@ struct Compactor {
   __device__ __forceinline__ void store(int j0, const uint4 (&buf)[kItems]) const {
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
-      const int item = it * kThreads + threadIdx.x;
+      const int item = it * kThreads + G::tid();
       const int row = item / (2 * kVecs), rem = item % (2 * kVecs);
       const int kv = rem / kVecs, vec = rem % kVecs;
       const int j = j0 + row;
@@ -171,29 +187,29 @@ struct Compactor {
 // place because idx is ascending (idx[j] >= j): chunk c writes ranks
 // [cW, (c+1)W) while chunk c+1 only reads positions >= (c+1)W, and the barrier
 // before chunk c+1's stores orders them after every read of chunks <= c+1.
-template <int kRowBytes>
+template <int kRowBytes, class G = CtaGroup>
 __device__ __forceinline__ void compact_rows(char* __restrict__ seg, const Geom& g,
                                              const int32_t* s_src, const int32_t* s_dst,
                                              const int32_t* idx, int K, int j_start) {
   constexpr int kItems = 4;
-  using C = Compactor<kRowBytes, kItems>;
+  using C = Compactor<kRowBytes, kItems, G>;
   const C c{seg, g, s_src, s_dst, idx, K, (int64_t)g.H * g.bs * kRowBytes};
   if (j_start >= K) return;
   uint4 a[kItems], b[kItems];
   int j0 = j_start;
   c.load(j0, a);
-  __syncthreads();
+  G::sync();
   while (true) {
     const int j1 = j0 + C::kChunk;
     if (j1 < K) c.load(j1, b);
     c.store(j0, a);
     if (j1 >= K) break;
-    __syncthreads();
+    G::sync();
     const int j2 = j1 + C::kChunk;
     if (j2 < K) c.load(j2, a);
     c.store(j1, b);
     if (j2 >= K) break;
-    __syncthreads();
+    G::sync();
     j0 = j2;
   }
 }

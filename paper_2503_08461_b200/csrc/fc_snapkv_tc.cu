@@ -1,19 +1,24 @@
 // fc_snapkv_tc.cu -- SnapKV scoring on the 5th-gen tensor cores (sm_100a).
 //
-// One CTA per (request, layer, kv-head) segment, 256 threads:
+// Persistent, warp-specialised: one CTA per SM walks a strided list of
+// (request, layer, kv-head) segments (longest requests first).
 //
-//   thread 0   TMA producer + MMA issuer: streams the segment's K tiles
-//              (128 tokens x D, fp16/bf16) from its paged blocks into a
-//              3-stage SMEM ring with cp.async.bulk.tensor (128-byte swizzle),
-//              and issues tcgen05.mma  S[tile] = K_tile . Q_win^T  (M=128
-//              tokens, N=w queries, K=D) into TMEM columns [tile*w, tile*w+w).
-//              The whole segment's window logits stay resident in TMEM
-//              (ceil(T/128)*w <= 512 columns, i.e. T <= 2048 at w = 32).
-//   all warps  epilogue from TMEM (tcgen05.ld 32x32b): per-query max, then
-//              sum of exp, then s'_t = mean_j softmax_j(t); avg-pool, window
-//              forced keep; then the shared segmented top-k and in-place
-//              compaction (fc_select.cuh).
+//   warp 0      TMA producer: loads the window queries (double-buffered) and
+//               streams every K tile (128 tokens x D, fp16/bf16) of every
+//               segment from its paged blocks into a 4-stage SMEM ring with
+//               cp.async.bulk.tensor (128-byte swizzle).
+//   warp 1      MMA issuer: tcgen05.mma  S[tile] = K_tile . Q_win^T
+//               (M = 128 tokens, N = 32 queries, K = D, fp32 accumulate) into
+//               a 16-slot TMEM ring (16 x 32 columns = all 512 columns). A
+//               segment's whole logit matrix stays resident (T <= 2048).
+//   warps 2-9   consumers (named barrier 1): per-query max, sum of exp and
+//               s'_t = mean_j softmax_j(t) straight from TMEM (tcgen05.ld,
+//               each warp group owns 16 of the 32 queries), freeing TMEM slots
+//               as they go; then avg-pool, forced window, segmented radix
+//               top-k and in-place compaction of K and V (fc_select.cuh).
 //
+// While the consumers finish segment s, the producer and MMA warps already
+// stream and multiply segment s+1 into the freed slots, so HBM stays busy.
 // K is read from HBM exactly once; scores never leave the SM. Precision:
 // fp16/bf16 products are exact in fp32, only the fp32 accumulation order
 // differs from the oracle (scores within 1e-5 relative, tests/test_gpu_press.py).
@@ -30,260 +35,325 @@
 
 namespace fc {
 
-constexpr int kTcStages = 3;
+constexpr int kTcStages = 4;
 constexpr int kTileM = 128;
+constexpr int kSlots = 16;                      // TMEM ring: 16 x 32 fp32 columns
+constexpr int kWin = 32;                        // window queries (UMMA N)
+constexpr int kConsumerFirst = 64;              // warps 0,1 = producer, MMA
+constexpr int kCompactorFirst = kConsumerFirst + kThreads;
+constexpr int kTcThreads = kCompactorFirst + kThreads;
+using Consumers = NamedGroup<kConsumerFirst, 1>;
+using Compactors = NamedGroup<kCompactorFirst, 2>;
 
-struct TcSmem {
-  int D, w, bs, max_T;
-  int tile_bytes, q_bytes;
-  int off_stage, off_q, off_tab, off_sc, off_s1, off_bar, total;
+struct CompactJob {  // consumer -> compactor hand-off of one segment
+  int32_t l, h, K, first_moved;
 };
 
-__host__ __device__ inline TcSmem tc_smem_plan(int D, int w, int bs, int max_T) {
+struct TcSmem {
+  int tile_bytes, q_bytes, max_nb;
+  int off_stage, off_q, off_ptab, off_ctab, off_idx, off_sc, off_s1, off_bar, total;
+};
+
+__host__ __device__ inline TcSmem tc_smem_plan(int D, int bs, int max_T) {
   TcSmem p;
-  p.D = D;
-  p.w = w;
-  p.bs = bs;
-  p.max_T = max_T;
   p.tile_bytes = kTileM * D * 2;
-  p.q_bytes = w * D * 2;
-  p.off_stage = 0;                                            // 1024-aligned base
+  p.q_bytes = (kWin * D * 2 + 1023) & ~1023;
+  p.max_nb = (max_T + bs - 1) / bs;
+  p.off_stage = 0;  // 1024-aligned base
   p.off_q = p.off_stage + kTcStages * p.tile_bytes;
-  p.off_tab = p.off_q + ((p.q_bytes + 1023) & ~1023);
-  const int nb = (max_T + bs - 1) / bs;
-  // Scores (sc) and window means (s1) live in the K stage ring: they are only
-  // written after the last MMA has consumed the last stage (mma_done).
-  p.off_sc = p.off_stage;
+  p.off_ptab = p.off_q + 2 * p.q_bytes;
+  p.off_ctab = p.off_ptab + ((p.max_nb * 4 + 15) & ~15);          // [2][max_nb]
+  p.off_idx = p.off_ctab + 2 * ((p.max_nb * 4 + 15) & ~15);        // [2][max_T]
+  p.off_sc = p.off_idx + 2 * ((max_T * 4 + 15) & ~15);
   p.off_s1 = p.off_sc + ((max_T * 4 + 15) & ~15);
-  p.off_bar = p.off_tab + ((nb * 4 + 15) & ~15);
-  p.total = p.off_bar + 16 * 8 + 1024;                        // barriers + alignment slack
+  p.off_bar = p.off_s1 + 2 * ((max_T * 4 + 15) & ~15);
+  p.total = p.off_bar + (2 * kTcStages + 8 + 2 * kSlots) * 8 + 1024;
   return p;
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kTcThreads, 1)
     snapkv_tc_kernel(char* __restrict__ arena, const int32_t* __restrict__ table, const Geom g,
                      const __grid_constant__ PressBatch b, const PressParams pp,
                      const __grid_constant__ CUtensorMap kmap,
-                     const __grid_constant__ CUtensorMap qmap, const fc_press_outputs out) {
-  constexpr int kHalves = D / 64;              // 128-byte K-dim slabs
-  constexpr int kKSteps = D / 16;              // UMMA_K = 16 for 16-bit inputs
-  constexpr int kFmt = sizeof(T) == 2 && Elem<T>::kDtype == FC_BF16 ? 1 : 0;
+                     const __grid_constant__ CUtensorMap qmap, const fc_press_outputs out,
+                     int n_items) {
+  constexpr int kHalves = D / 64;  // 128-byte K-dim slabs
+  constexpr int kKSteps = D / 16;  // UMMA_K = 16 for 16-bit inputs
+  constexpr int kFmt = Elem<T>::kDtype == FC_BF16 ? 1 : 0;
   extern __shared__ unsigned char smem_raw[];
   __shared__ SelectScratch ss;
   __shared__ uint32_t s_tmem;
-  __shared__ float s_red[kWarps][32];
-  __shared__ float s_m[32], s_zinv[32];
+  __shared__ float s_red[kWarps][16];
+  __shared__ float s_m[kWin], s_zinv[kWin];
 
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  const int w = pp.window;
-  const TcSmem plan = tc_smem_plan(D, w, g.bs, b.max_T);
+  const TcSmem plan = tc_smem_plan(D, g.bs, b.max_T);
   unsigned char* stages = smem + plan.off_stage;
-  unsigned char* qs = smem + plan.off_q;
-  int32_t* s_tab = reinterpret_cast<int32_t*>(smem + plan.off_tab);
+  unsigned char* qbuf = smem + plan.off_q;
+  int32_t* ptab = reinterpret_cast<int32_t*>(smem + plan.off_ptab);
+  const int nb_stride = ((plan.max_nb * 4 + 15) & ~15) / 4;
+  const int t_stride = ((b.max_T * 4 + 15) & ~15) / 4;
+  int32_t* ctab = reinterpret_cast<int32_t*>(smem + plan.off_ctab);   // [2][nb_stride]
+  int32_t* idxbuf = reinterpret_cast<int32_t*>(smem + plan.off_idx);  // [2][t_stride]
+  __shared__ CompactJob s_job[2];
   float* sc = reinterpret_cast<float*>(smem + plan.off_sc);
-  float* s1 = reinterpret_cast<float*>(smem + plan.off_s1);
+  float* s1 = reinterpret_cast<float*>(smem + plan.off_s1);  // [2][max_T]
+  const int s1_stride = ((b.max_T * 4 + 15) & ~15) / 4;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + plan.off_bar);
-  uint64_t* full = bars;                 // [kTcStages]
-  uint64_t* empty = bars + kTcStages;    // [kTcStages]
+  uint64_t* st_full = bars;
+  uint64_t* st_empty = bars + kTcStages;
   uint64_t* q_full = bars + 2 * kTcStages;
-  uint64_t* mma_done = q_full + 1;
+  uint64_t* q_empty = q_full + 2;
+  uint64_t* job_full = q_empty + 2;
+  uint64_t* job_empty = job_full + 2;
+  uint64_t* sl_full = job_empty + 2;
+  uint64_t* sl_empty = sl_full + kSlots;
 
-  const int LH = g.L * g.H;
-  const int r = blockIdx.x / LH, lh = blockIdx.x % LH;
-  const int l = lh / g.H, h = lh % g.H;
-  const PressReq q = b.req[r];
-  const int T_len = q.T, K = q.K;
-  const int nb = (T_len + g.bs - 1) / g.bs;
-  const int ntiles = (T_len + kTileM - 1) / kTileM;
-  uint32_t ncols = 32;
-  while (ncols < (uint32_t)(ntiles * w)) ncols <<= 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  for (int i = threadIdx.x; i < nb; i += kThreads) s_tab[i] = table[(int64_t)q.slot * g.max_bpr + i];
+  const int LH = g.L * g.H;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2 * kTcStages + 2; ++i) tc::mbar_init(&bars[i], 1);
+    for (int i = 0; i < 2 * kTcStages + 8 + kSlots; ++i) tc::mbar_init(&bars[i], 1);
+    for (int i = 0; i < kSlots; ++i) tc::mbar_init(&sl_empty[i], kWarps);  // one arrive per consumer warp
     tc::fence_barrier_init();
-    ss.first_drop = INT_MAX;
     tc::tma_prefetch_desc(&kmap);
     tc::tma_prefetch_desc(&qmap);
   }
-  if (warp == 1) tc::tmem_alloc(&s_tmem, ncols);
+  if (warp == 1) tc::tmem_alloc(&s_tmem, kSlots * kWin);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = s_tmem;
 
-  // ---- producer + MMA issuer (one thread) ----
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
+    // ================= TMA producer =================
     const int chunks = kTileM / g.bs;
-    const int64_t row_l = (int64_t)l * g.num_blocks * 2 * g.H * g.bs + (int64_t)h * g.bs;
-    auto issue_tile = [&](int k, int st) {
-      int n_chunks = min(chunks, nb - k * chunks);
-      tc::mbar_expect_tx(&full[st], (uint32_t)(n_chunks * g.bs * D * 2));
-      unsigned char* dst = stages + st * plan.tile_bytes;
-      for (int c = 0; c < n_chunks; ++c) {
-        const int64_t row0 = row_l + (int64_t)s_tab[k * chunks + c] * 2 * g.H * g.bs;
+    int gtile = 0;
+    for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
+      const int r = item / LH, lh = item % LH, l = lh / g.H, h = lh % g.H;
+      const PressReq q = b.req[r];
+      const int nb = (q.T + g.bs - 1) / g.bs, ntiles = (q.T + kTileM - 1) / kTileM;
+      __syncwarp();
+      for (int i = lane; i < nb; i += 32) ptab[i] = table[(int64_t)q.slot * g.max_bpr + i];
+      __syncwarp();
+      if (lane == 0) {
+        const int qb = it & 1;
+        tc::mbar_wait(&q_empty[qb], ((it >> 1) & 1) ^ 1);
+        const int qrow = (int)((((int64_t)q.q_idx * g.L + l) * pp.num_q_heads + h) * kWin);
+        tc::mbar_expect_tx(&q_full[qb], (uint32_t)(kWin * D * 2));
 #pragma unroll
         for (int hf = 0; hf < kHalves; ++hf)
-          tc::tma_load_2d(dst + hf * kTileM * 128 + c * g.bs * 128, &kmap, &full[st], hf * 64,
-                          (int)row0);
-      }
-    };
-    // window queries of this (request, layer, kv-head): rows [qrow, qrow + w)
-    const int qrow = (int)(((int64_t)q.q_idx * g.L + l) * pp.num_q_heads + h) * w;
-    tc::mbar_expect_tx(q_full, (uint32_t)(w * D * 2));
+          tc::tma_load_2d(qbuf + qb * plan.q_bytes + hf * kWin * 128, &qmap, &q_full[qb], hf * 64, qrow);
+        const int64_t row_l = (int64_t)l * g.num_blocks * 2 * g.H * g.bs + (int64_t)h * g.bs;
+        for (int k = 0; k < ntiles; ++k, ++gtile) {
+          const int st = gtile % kTcStages;
+          tc::mbar_wait(&st_empty[st], ((gtile / kTcStages) & 1) ^ 1);
+          const int n_chunks = min(chunks, nb - k * chunks);
+          tc::mbar_expect_tx(&st_full[st], (uint32_t)(n_chunks * g.bs * D * 2));
+          unsigned char* dst = stages + st * plan.tile_bytes;
+          for (int c = 0; c < n_chunks; ++c) {
+            const int64_t row0 = row_l + (int64_t)ptab[k * chunks + c] * 2 * g.H * g.bs;
 #pragma unroll
-    for (int hf = 0; hf < kHalves; ++hf) tc::tma_load_2d(qs + hf * w * 128, &qmap, q_full, hf * 64, qrow);
-    for (int k = 0; k < min(kTcStages, ntiles); ++k) issue_tile(k, k);
-    tc::mbar_wait(q_full, 0);
-    const uint32_t idesc = tc::idesc_f16(kFmt, kTileM, w);
-    const uint32_t q_base = tc::smem_u32(qs);
-    for (int k = 0; k < ntiles; ++k) {
-      const int st = k % kTcStages;
-      const uint32_t ph = (uint32_t)(k / kTcStages) & 1u;
-      tc::mbar_wait(&full[st], ph);
-      tc::fence_after_sync();
-      const uint32_t a_base = tc::smem_u32(stages + st * plan.tile_bytes);
-#pragma unroll
-      for (int kk = 0; kk < kKSteps; ++kk) {
-        const uint32_t koff = (uint32_t)((kk & 3) * 32);
-        const uint64_t ad = tc::desc_k_sw128(a_base + (kk >> 2) * kTileM * 128 + koff);
-        const uint64_t bd = tc::desc_k_sw128(q_base + (kk >> 2) * w * 128 + koff);
-        tc::mma_f16(tmem + (uint32_t)(k * w), ad, bd, idesc, kk > 0 ? 1u : 0u);
-      }
-      tc::mma_commit(&empty[st]);
-      if (k + kTcStages < ntiles) {
-        tc::mbar_wait(&empty[st], ph);
-        issue_tile(k + kTcStages, st);
+            for (int hf = 0; hf < kHalves; ++hf)
+              tc::tma_load_2d(dst + hf * kTileM * 128 + c * g.bs * 128, &kmap, &st_full[st],
+                              hf * 64, (int)row0);
+          }
+        }
+      } else {
+        gtile += ntiles;
       }
     }
-    tc::mma_commit(mma_done);
-  }
-  __syncwarp();
-  tc::mbar_wait(mma_done, 0);
-  tc::fence_after_sync();
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_f16(kFmt, kTileM, kWin);
+      int gtile = 0;
+      for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
+        const PressReq q = b.req[item / LH];
+        const int ntiles = (q.T + kTileM - 1) / kTileM;
+        const int qb = it & 1;
+        tc::mbar_wait(&q_full[qb], (it >> 1) & 1);
+        const uint32_t q_base = tc::smem_u32(qbuf + qb * plan.q_bytes);
+        for (int k = 0; k < ntiles; ++k, ++gtile) {
+          const int st = gtile % kTcStages, sl = gtile % kSlots;
+          tc::mbar_wait(&sl_empty[sl], ((gtile / kSlots) & 1) ^ 1);
+          tc::mbar_wait(&st_full[st], (gtile / kTcStages) & 1);
+          tc::fence_after_sync();
+          const uint32_t a_base = tc::smem_u32(stages + st * plan.tile_bytes);
+#pragma unroll
+          for (int kk = 0; kk < kKSteps; ++kk) {
+            const uint32_t koff = (uint32_t)((kk & 3) * 32);
+            const uint64_t ad = tc::desc_k_sw128(a_base + (kk >> 2) * kTileM * 128 + koff);
+            const uint64_t bd = tc::desc_k_sw128(q_base + (kk >> 2) * kWin * 128 + koff);
+            tc::mma_f16(tmem + (uint32_t)(sl * kWin), ad, bd, idesc, kk > 0 ? 1u : 0u);
+          }
+          tc::mma_commit(&st_empty[st]);
+          tc::mma_commit(&sl_full[sl]);
+        }
+        tc::mma_commit(&q_empty[qb]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kCompactorFirst / 32) {
+    // ================= compactors (8 warps, named barrier 2) =================
+    for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
+      const int jb = it & 1;
+      tc::mbar_wait(&job_full[jb], (it >> 1) & 1);
+      const CompactJob job = s_job[jb];
+      char* seg = arena + g.seg_base(job.l, 0, job.h);
+      compact_rows<D * (int)sizeof(T), Compactors>(seg, g, ctab + jb * nb_stride,
+                                                   ctab + jb * nb_stride, idxbuf + jb * t_stride,
+                                                   job.K, job.first_moved);
+      Compactors::sync();
+      if (Compactors::tid() == 0) tc::mbar_arrive(&job_empty[jb]);
+    }
+  } else {
+    // ================= consumers (8 warps, named barrier 1) =================
+    const int cw = warp - 2;                 // consumer warp 0..7
+    const int grp = cw >> 2;                 // owns queries [16*grp, 16*grp + 16)
+    const int quarter = warp & 3;            // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(grp * 16);
+    // logits in the log2 domain: a_jt * log2(e) = acc * (log2(e) / sqrt(D))
+    const float scale = 1.4426950408889634f / sqrtf((float)D);
+    const int ct = Consumers::tid();
+    int gtile = 0;
+    for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
+      const int r = item / LH, lh = item % LH, l = lh / g.H, h = lh % g.H;
+      const PressReq q = b.req[r];
+      const int T_len = q.T, K = q.K;
+      const int nb = (T_len + g.bs - 1) / g.bs, ntiles = (T_len + kTileM - 1) / kTileM;
+      const int n_keep = T_len - kWin;
+      const int jb = it & 1;
+      if (ct == 0) ss.first_drop = INT_MAX;
 
-  // ---- epilogue: softmax over all T per window query, from TMEM ----
-  const float inv_sqrt_d = 1.0f / sqrtf((float)D);
-  const int quarter = warp & 3, parity = warp >> 2;
-  const int row = quarter * 32 + lane;
-  const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-  const int n_keep = T_len - w;
-  float acc[32];
-  // pass 1: per-query max
+      float acc[16];
+      // pass 1: per-query max over all tokens
 #pragma unroll
-  for (int j = 0; j < 32; ++j) acc[j] = -INFINITY;
-  for (int k = parity; k < ntiles; k += 2) {
-    float v[32];
-    tc::tmem_ld_32x32b_x32(lane_addr + (uint32_t)(k * w), v);
-    const int t = k * kTileM + row;
+      for (int j = 0; j < 16; ++j) acc[j] = -INFINITY;
+      for (int k = 0; k < ntiles; ++k) {
+        const int sl = (gtile + k) % kSlots;
+        tc::mbar_wait(&sl_full[sl], ((gtile + k) / kSlots) & 1);
+        tc::fence_after_sync();
+        float v[16];
+        tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+        const int t = k * kTileM + row;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const bool ok = j < w && t < T_len && t <= T_len - w + j;
-      if (ok) acc[j] = fmaxf(acc[j], v[j] * inv_sqrt_d);
-    }
-  }
+        for (int j = 0; j < 16; ++j)
+          if (t < T_len && t <= T_len - kWin + grp * 16 + j) acc[j] = fmaxf(acc[j], v[j] * scale);
+      }
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
+      for (int j = 0; j < 16; ++j)
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) acc[j] = fmaxf(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], off));
+        for (int off = 16; off >= 1; off >>= 1) acc[j] = fmaxf(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], off));
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
-    if (lane == j) s_red[warp][j] = acc[j];
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float m = s_red[0][threadIdx.x];
-    for (int i = 1; i < kWarps; ++i) m = fmaxf(m, s_red[i][threadIdx.x]);
-    s_m[threadIdx.x] = m;
-  }
-  __syncthreads();
-  float mj[32];
+      for (int j = 0; j < 16; ++j)
+        if (lane == j) s_red[cw][j] = acc[j];
+      Consumers::sync();
+      if (ct < kWin) {
+        const int gg = ct >> 4, jj = ct & 15;
+        float m = s_red[4 * gg][jj];
+        for (int i = 1; i < 4; ++i) m = fmaxf(m, s_red[4 * gg + i][jj]);
+        s_m[ct] = m;
+      }
+      Consumers::sync();
+      float mj[16];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) mj[j] = s_m[j];
-  // pass 2: per-query sum of exp
+      for (int j = 0; j < 16; ++j) mj[j] = s_m[grp * 16 + j];
+      // pass 2: per-query sum of exp
 #pragma unroll
-  for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-  for (int k = parity; k < ntiles; k += 2) {
-    float v[32];
-    tc::tmem_ld_32x32b_x32(lane_addr + (uint32_t)(k * w), v);
-    const int t = k * kTileM + row;
+      for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+      for (int k = 0; k < ntiles; ++k) {
+        const int sl = (gtile + k) % kSlots;
+        float v[16];
+        tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+        const int t = k * kTileM + row;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const bool ok = j < w && t < T_len && t <= T_len - w + j;
-      if (ok) acc[j] += expf(v[j] * inv_sqrt_d - mj[j]);
-    }
-  }
+        for (int j = 0; j < 16; ++j)
+          if (t < T_len && t <= T_len - kWin + grp * 16 + j) acc[j] += tc::ex2(fmaf(v[j], scale, -mj[j]));
+      }
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
+      for (int j = 0; j < 16; ++j)
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+        for (int off = 16; off >= 1; off >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
-    if (lane == j) s_red[warp][j] = acc[j];
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float z = 0.f;
-    for (int i = 0; i < kWarps; ++i) z += s_red[i][threadIdx.x];
-    s_zinv[threadIdx.x] = 1.0f / z;
-  }
-  __syncthreads();
-  float zj[32];
+      for (int j = 0; j < 16; ++j)
+        if (lane == j) s_red[cw][j] = acc[j];
+      Consumers::sync();
+      if (ct < kWin) {
+        const int gg = ct >> 4, jj = ct & 15;
+        float z = 0.f;
+        for (int i = 0; i < 4; ++i) z += s_red[4 * gg + i][jj];
+        s_zinv[ct] = 1.0f / z;
+      }
+      Consumers::sync();
+      float zj[16];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) zj[j] = s_zinv[j];
-  // pass 3: s'_t = mean over the window of the normalised probabilities
-  for (int k = parity; k < ntiles; k += 2) {
-    float v[32];
-    tc::tmem_ld_32x32b_x32(lane_addr + (uint32_t)(k * w), v);
-    const int t = k * kTileM + row;
-    if (t < n_keep) {
-      float s = 0.f;
+      for (int j = 0; j < 16; ++j) zj[j] = s_zinv[grp * 16 + j];
+      // pass 3: partial window mean of the normalised probabilities; frees TMEM slots
+      for (int k = 0; k < ntiles; ++k) {
+        const int sl = (gtile + k) % kSlots;
+        float v[16];
+        tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
+        const int t = k * kTileM + row;
+        if (t < n_keep) {
+          float s = 0.f;
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < w && t <= T_len - w + j) s += expf(v[j] * inv_sqrt_d - mj[j]) * zj[j];
-      s1[t] = s / (float)w;
+          for (int j = 0; j < 16; ++j)
+            if (t <= T_len - kWin + grp * 16 + j) s += tc::ex2(fmaf(v[j], scale, -mj[j])) * zj[j];
+          s1[grp * s1_stride + t] = s;
+        }
+      }
+      gtile += ntiles;
+      Consumers::sync();
+      // avg-pool (zero pad, count_include_pad), forced window
+      const int half = pp.pool_kernel / 2;
+      for (int t = ct; t < T_len; t += kThreads) {
+        float v = INFINITY;
+        if (t < n_keep) {
+          float a = 0.f;
+          for (int o = -half; o <= half; ++o) {
+            const int u = t + o;
+            a += (u >= 0 && u < n_keep) ? (s1[u] + s1[s1_stride + u]) / (float)kWin : 0.f;
+          }
+          v = a / (float)pp.pool_kernel;
+        }
+        sc[t] = v;
+      }
+      Consumers::sync();
+      if (out.scores) {
+        float* so = out.scores + q.score_off + (int64_t)lh * T_len;
+        for (int t = ct; t < T_len; t += kThreads) so[t] = sc[t];
+      }
+      uint32_t* keys = reinterpret_cast<uint32_t*>(sc);
+      for (int t = ct; t < T_len; t += kThreads) keys[t] = float_key(sc[t]);
+      Consumers::sync();
+      // hand the kept list to the compactors (double-buffered)
+      tc::mbar_wait(&job_empty[jb], ((it >> 1) & 1) ^ 1);
+      int32_t* idx = idxbuf + jb * t_stride;
+      for (int i = ct; i < nb; i += kThreads) ctab[jb * nb_stride + i] = table[(int64_t)q.slot * g.max_bpr + i];
+      if (b.per_segment && q.seg0 < T_len) {
+        select_emit<Consumers>(keys, q.seg0, q.K0, idx, 0, 0, ss);
+        select_emit<Consumers>(keys + q.seg0, T_len - q.seg0, K - q.K0, idx, q.K0, q.seg0, ss);
+      } else {
+        select_emit<Consumers>(keys, T_len, K, idx, 0, 0, ss);
+      }
+      if (out.kept_idx) {
+        int32_t* ko = out.kept_idx + q.kept_off + (int64_t)lh * K;
+        for (int j = ct; j < K; j += kThreads) ko[j] = idx[j];
+      }
+      if (ct == 0) s_job[jb] = CompactJob{l, h, K, min(ss.first_drop, K)};
+      Consumers::sync();  // idx, ctab, job complete; sc / ss reused by the next segment
+      if (ct == 0) tc::mbar_arrive(&job_full[jb]);
     }
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tmem, ncols);
-
-  // ---- avg-pool (zero pad), forced window, then the shared select + compact ----
-  const int half = pp.pool_kernel / 2;
-  for (int t = threadIdx.x; t < T_len; t += kThreads) {
-    float v = INFINITY;
-    if (t < n_keep) {
-      float a = 0.f;
-      for (int o = -half; o <= half; ++o) {
-        const int u = t + o;
-        a += (u >= 0 && u < n_keep) ? s1[u] : 0.f;
-      }
-      v = a / (float)pp.pool_kernel;
-    }
-    sc[t] = v;
-  }
-  __syncthreads();
-  if (out.scores) {
-    float* so = out.scores + q.score_off + (int64_t)lh * T_len;
-    for (int t = threadIdx.x; t < T_len; t += kThreads) so[t] = sc[t];
-  }
-  uint32_t* keys = reinterpret_cast<uint32_t*>(sc);
-  for (int t = threadIdx.x; t < T_len; t += kThreads) keys[t] = float_key(sc[t]);
-  __syncthreads();
-  int32_t* idx = reinterpret_cast<int32_t*>(sc);
-  if (b.per_segment && q.seg0 < T_len) {
-    select_emit(keys, q.seg0, q.K0, idx, 0, 0, ss);
-    select_emit(keys + q.seg0, T_len - q.seg0, K - q.K0, idx, q.K0, q.seg0, ss);
-  } else {
-    select_emit(keys, T_len, K, idx, 0, 0, ss);
-  }
-  if (out.kept_idx) {
-    int32_t* ko = out.kept_idx + q.kept_off + (int64_t)lh * K;
-    for (int j = threadIdx.x; j < K; j += kThreads) ko[j] = idx[j];
-  }
-  char* seg = arena + g.seg_base(l, 0, h);
-  compact_rows<D * (int)sizeof(T)>(seg, g, s_tab, s_tab, idx, K, min(ss.first_drop, K));
+  if (warp == 1) tc::tmem_dealloc(tmem, kSlots * kWin);
 }
 
 // ---------------------------------------------------------------------------
@@ -329,7 +399,8 @@ bool snapkv_tc_supported(const Geom& g, int dtype, const PressParams& pp, int ma
   if (pp.num_q_heads != g.H) return false;          // one query head per kv head
   if (pp.window != 32) return false;               // one 32x32b.x32 TMEM load per tile
   if (g.bs < 8 || g.bs > 128) return false;
-  if ((max_T + kTileM - 1) / kTileM * pp.window > 512) return false;
+  if ((max_T + kTileM - 1) / kTileM > kSlots) return false;         // whole segment in TMEM
+  if (tc_smem_plan(g.D, g.bs, max_T).total > 227 * 1024) return false;
   return true;
 }
 
@@ -344,12 +415,16 @@ fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t*
   st = encode_rows(&qmap, in.q_window, dtype, g.D,
                    (uint64_t)n_requests_total * g.L * pp.num_q_heads * pp.window, pp.window);
   if (st != FC_OK) return st;
-  const TcSmem plan = tc_smem_plan(g.D, pp.window, g.bs, b.max_T);
+  const TcSmem plan = tc_smem_plan(g.D, g.bs, b.max_T);
   const int n_items = b.n * g.L * g.H;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = n_items < sms ? n_items : sms;
   auto launch = [&](auto kern) -> fc_status {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.total);
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(snapkv_tc)");
-    kern<<<n_items, kThreads, plan.total, stream>>>(arena, table, g, b, pp, kmap, qmap, out);
+    kern<<<grid, kTcThreads, plan.total, stream>>>(arena, table, g, b, pp, kmap, qmap, out, n_items);
     note_launch();
     return cuda_check(cudaGetLastError(), "snapkv_tc_kernel");
   };
