@@ -187,11 +187,10 @@ struct Compactor {
 // place because idx is ascending (idx[j] >= j): chunk c writes ranks
 // [cW, (c+1)W) while chunk c+1 only reads positions >= (c+1)W, and the barrier
 // before chunk c+1's stores orders them after every read of chunks <= c+1.
-template <int kRowBytes, class G = CtaGroup>
+template <int kRowBytes, class G = CtaGroup, int kItems = 4>
 __device__ __forceinline__ void compact_rows(char* __restrict__ seg, const Geom& g,
                                              const int32_t* s_src, const int32_t* s_dst,
                                              const int32_t* idx, int K, int j_start) {
-  constexpr int kItems = 4;
   using C = Compactor<kRowBytes, kItems, G>;
   const C c{seg, g, s_src, s_dst, idx, K, (int64_t)g.H * g.bs * kRowBytes};
   if (j_start >= K) return;

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc::mbar_wait(&job_full[jb], (it >> 1) & 1);
       const CompactJob job = s_job[jb];
       char* seg = arena + g.seg_base(job.l, 0, job.h);
-      compact_rows<D * (int)sizeof(T), Compactors>(seg, g, ctab + jb * nb_stride,
+      compact_rows<D * (int)sizeof(T), Compactors, 8>(seg, g, ctab + jb * nb_stride,
                                                    ctab + jb * nb_stride, idxbuf + jb * t_stride,
                                                    job.K, job.first_moved);
       Compactors::sync();
