@@ -320,3 +320,19 @@ def test_chunk_press_in_pool(cuda, map_kind, dtype):
                         np.testing.assert_allclose(g32, want32, rtol=1e-2 if dtype != "float32" else 1e-6,
                                                    atol=1e-6)
     pool.verify_conservation()
+
+
+def test_churn_waves_conserve_and_free_everything(cuda):
+    from paper_2503_08461_b200 import churn
+
+    cfg = _model("float16", 2, 2, 128)
+    specs = [split_modalities(576, t) for t in (100, 700, 33, 1500, 9, 400, 1200, 64)]
+    pool = KVCachePool(cfg, 2500 * cfg.bytes_per_token, device=cuda, kv_dtype="float16",
+                       max_handles=64, max_tokens_per_handle=4096)
+    comp = CompressorSpec(factor=4, press=PressKind.KNORM)
+    st = churn.run_waves(pool, specs, comp, lambda n: {}, decode_tokens=8)
+    assert st.compressed_requests == len(specs) and st.waves >= 3
+    assert st.raw_tokens == sum(s.total_tokens for s in specs)
+    bs = pool.block_stats()
+    assert pool.current_bytes == 0 and bs.used_blocks == 0 and bs.free_blocks == bs.num_blocks
+    assert 0.0 <= st.max_fragmentation < 1.0
