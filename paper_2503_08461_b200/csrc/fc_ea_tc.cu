@@ -1,0 +1,484 @@
+// fc_ea_tc.cu -- ExpectedAttention scoring on the 5th-gen tensor cores (sm_100a).
+//
+//   z_t = mu . K_t / sqrt(D) + K_t^T Sigma K_t / (2D),  p = softmax_{t >= n_sink}(z),
+//   s_t = p_t * ||V_t||,  s_{t < n_sink} = +inf
+//
+// Persistent and warp-specialised like fc_snapkv_tc.cu. Per (request, layer,
+// kv-head) segment the tensor cores compute Y = K_tile . B^T with
+//   B = [ Sigma^T ; mu ; 0 ]   (144 x D, fp16),  D_tile[t][n<128] = (K Sigma)[t][n],
+//                                                D_tile[t][128]  = K_t . mu,
+// where Sigma and mu (fp32 inputs) are split into fp16 hi + lo parts and both
+// halves accumulate into the same TMEM tile (~2^-22 relative per element; K
+// in fp16 is exact). The consumer warps finish q_t = sum_n Y[t][n] K[t][n]
+// in fp32 from the K rows still in SMEM.
+//
+//   warp 0     TMA producer. Per segment the SMEM ring carries, in order:
+//              the segment's K tiles, the NEXT segment's Sigma (2 x 32 KB fp32
+//              stages), then the segment's V tiles (for ||V_t||).
+//   warp 1     MMA issuer: 2 x 8 tcgen05.mma (M=128, N=144, K=16) per K tile
+//              into a 2-slot TMEM ring (2 x 256 columns).
+//   warps 2-9  consumers: Sigma -> B conversion (hi/lo split, transpose,
+//              128-byte swizzle), z_t epilogue from TMEM + SMEM, softmax,
+//              V norms, segmented radix top-k -> hand-off.
+//   warps 10-17 compactors: in-place compaction of kept K/V rows.
+//
+// Algorithmic bytes per segment: R + 2C + (D + D^2) * 4.
+#include <cudaTypedefs.h>
+
+#include <cfloat>
+#include <climits>
+#include <cstring>
+#include <mutex>
+
+#include "fc_select.cuh"
+#include "fc_tc.cuh"
+
+namespace fc {
+
+namespace ea {
+
+constexpr int kD = 128;
+constexpr int kStages = 3;
+constexpr int kTileM = 128;
+constexpr int kBRows = 144;                     // 128 Sigma^T rows + mu + 15 zero rows
+constexpr int kSlotCols = 256;                  // TMEM slot stride (N = 144 used)
+constexpr int kSlots = 2;
+constexpr int kStageBytes = kTileM * kD * 2;    // 32 KB: one K/V tile or half of Sigma (fp32)
+constexpr int kBHalf = kBRows * 128;            // one 64-column slab of B (bytes)
+constexpr int kBBytes = 2 * kBHalf;             // one full B matrix (hi or lo)
+constexpr int kConsumerFirst = 64;
+constexpr int kCompactorFirst = kConsumerFirst + kThreads;
+constexpr int kEaThreads = kCompactorFirst + kThreads;
+using Consumers = NamedGroup<kConsumerFirst, 1>;
+using Compactors = NamedGroup<kCompactorFirst, 2>;
+
+struct Job {
+  int32_t l, h, K, first_moved;
+};
+
+struct Smem {
+  int max_nb, max_K;
+  int off_ring, off_b, off_zt, off_idx, off_ctab, off_bar, total;
+};
+
+__host__ __device__ inline Smem plan(int bs, int max_T, int max_K) {
+  Smem p;
+  p.max_nb = (max_T + bs - 1) / bs;
+  p.max_K = max_K;
+  p.off_ring = 0;
+  p.off_b = p.off_ring + kStages * kStageBytes;
+  p.off_zt = p.off_b + 2 * kBBytes;
+  p.off_idx = p.off_zt + ((max_T * 4 + 15) & ~15);
+  p.off_ctab = p.off_idx + 2 * ((max_K * 4 + 15) & ~15);
+  p.off_bar = p.off_ctab + 2 * ((p.max_nb * 4 + 15) & ~15);
+  p.total = p.off_bar + 64 * 8 + 1024;
+  return p;
+}
+
+// Positions of one segment's stages in the global FIFO ring sequence:
+//   [Sigma(first) x2] then per segment: [K tiles][Sigma(next) x2 if any][V tiles].
+struct SegPos {
+  int k0, sig_next, v0, next;
+};
+__device__ __forceinline__ SegPos seg_pos(int start, int ntiles, bool has_next) {
+  SegPos s;
+  s.k0 = start;
+  s.sig_next = start + ntiles;
+  s.v0 = s.sig_next + (has_next ? 2 : 0);
+  s.next = s.v0 + ntiles;
+  return s;
+}
+
+// byte offset of B[n][k] (fp16) in the 128B-swizzled K-major layout
+__device__ __forceinline__ int b_off(int n, int k) {
+  const int half = k >> 6, c = (k & 63) >> 3, e = k & 7, r = n & 7;
+  return half * kBHalf + (n >> 3) * 1024 + r * 128 + ((c ^ r) << 4) + e * 2;
+}
+
+}  // namespace ea
+
+using namespace ea;
+
+__global__ void __launch_bounds__(kEaThreads, 1)
+    ea_tc_kernel(char* __restrict__ arena, const int32_t* __restrict__ table, const Geom g,
+                 const __grid_constant__ PressBatch b, const PressParams pp,
+                 const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap cmap,
+                 const float* __restrict__ mean_q, const fc_press_outputs out, int n_items,
+                 int max_K) {
+  extern __shared__ unsigned char smem_raw[];
+  __shared__ SelectScratch ss;
+  __shared__ uint32_t s_tmem;
+  __shared__ Job s_job[2];
+  __shared__ float s_stat[2];
+
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const Smem P = plan(g.bs, b.max_T, max_K);
+  unsigned char* ring = smem + P.off_ring;
+  unsigned char* bmat = smem + P.off_b;  // [hi | lo]
+  float* zt = reinterpret_cast<float*>(smem + P.off_zt);
+  const int k_stride = ((max_K * 4 + 15) & ~15) / 4;
+  const int nb_stride = ((P.max_nb * 4 + 15) & ~15) / 4;
+  int32_t* idxbuf = reinterpret_cast<int32_t*>(smem + P.off_idx);
+  int32_t* ctab = reinterpret_cast<int32_t*>(smem + P.off_ctab);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.off_bar);
+  uint64_t* st_full = bars;                  // [kStages]
+  uint64_t* st_empty = bars + kStages;       // [kStages] 8 arrivals (consumer warps)
+  uint64_t* sl_full = bars + 2 * kStages;    // [kSlots]
+  uint64_t* sl_empty = sl_full + kSlots;     // [kSlots] 8 arrivals
+  uint64_t* b_full = sl_empty + kSlots;
+  uint64_t* b_empty = b_full + 1;
+  uint64_t* job_full = b_empty + 1;          // [2]
+  uint64_t* job_empty = job_full + 2;        // [2]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int LH = g.L * g.H;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      tc::mbar_init(&st_full[i], 1);
+      tc::mbar_init(&st_empty[i], kWarps);
+    }
+    for (int i = 0; i < kSlots; ++i) {
+      tc::mbar_init(&sl_full[i], 1);
+      tc::mbar_init(&sl_empty[i], kWarps);
+    }
+    tc::mbar_init(b_full, 1);
+    tc::mbar_init(b_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&job_full[i], 1);
+      tc::mbar_init(&job_empty[i], 1);
+    }
+    tc::fence_barrier_init();
+    tc::tma_prefetch_desc(&kmap);
+    tc::tma_prefetch_desc(&cmap);
+  }
+  // zero the B rows that carry no data (129..143 of hi and lo) once
+  for (int i = threadIdx.x; i < 2 * 2 * 16 * 128 / 16; i += blockDim.x) {
+    const int mat = i / (2 * 16 * 8), rem = i % (2 * 16 * 8);
+    const int half = rem / (16 * 8), rr = rem % (16 * 8);
+    const int n = 128 + rr / 8, c = rr % 8;
+    *reinterpret_cast<uint4*>(bmat + mat * kBBytes + half * kBHalf + (n >> 3) * 1024 + (n & 7) * 128 + (c << 4)) =
+        make_uint4(0, 0, 0, 0);
+  }
+  if (warp == 1) tc::tmem_alloc(&s_tmem, kSlots * kSlotCols);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = s_tmem;
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      const int chunks = kTileM / g.bs;
+      int pos = 0;
+      auto acquire = [&](int p) -> unsigned char* {
+        const int st = p % kStages;
+        tc::mbar_wait(&st_empty[st], ((p / kStages) & 1) ^ 1);
+        return ring + st * kStageBytes;
+      };
+      auto load_sigma = [&](int item) {
+        const PressReq q = b.req[item / LH];
+        const int lh = item % LH, l = lh / g.H, h = lh % g.H;
+        const int row = (int)((((int64_t)q.q_idx * g.L + l) * pp.num_q_heads + h) * kD);
+        for (int part = 0; part < 2; ++part, ++pos) {
+          unsigned char* dst = acquire(pos);
+          uint64_t* bar = &st_full[pos % kStages];
+          tc::mbar_expect_tx(bar, 64 * kD * 4);
+          tc::tma_load_2d(dst, &cmap, bar, 0, row + part * 64);
+        }
+      };
+      auto load_tiles = [&](const PressReq& q, int l, int h, int kv) {
+        const int nb = (q.T + g.bs - 1) / g.bs, ntiles = (q.T + kTileM - 1) / kTileM;
+        const int64_t row_l = ((int64_t)l * g.num_blocks * 2 + kv) * g.H * g.bs + (int64_t)h * g.bs;
+        for (int k = 0; k < ntiles; ++k, ++pos) {
+          unsigned char* dst = acquire(pos);
+          uint64_t* bar = &st_full[pos % kStages];
+          const int n_chunks = min(chunks, nb - k * chunks);
+          tc::mbar_expect_tx(bar, (uint32_t)(n_chunks * g.bs * kD * 2));
+          for (int c = 0; c < n_chunks; ++c) {
+            const int blk = table[(int64_t)q.slot * g.max_bpr + k * chunks + c];
+            const int64_t row0 = row_l + (int64_t)blk * 2 * g.H * g.bs;
+            tc::tma_load_2d(dst + c * g.bs * 128, &kmap, bar, 0, (int)row0);
+            tc::tma_load_2d(dst + kTileM * 128 + c * g.bs * 128, &kmap, bar, 64, (int)row0);
+          }
+        }
+      };
+      if ((int)blockIdx.x < n_items) load_sigma(blockIdx.x);
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int lh = item % LH, l = lh / g.H, h = lh % g.H;
+        const PressReq q = b.req[item / LH];
+        load_tiles(q, l, h, 0);
+        if (item + (int)gridDim.x < n_items) load_sigma(item + gridDim.x);
+        load_tiles(q, l, h, 1);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_f16(0, kTileM, kBRows);
+      const uint32_t bh = tc::smem_u32(bmat), bl = bh + kBBytes;
+      int pos = 2, gt = 0;
+      for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
+        const PressReq q = b.req[item / LH];
+        const int ntiles = (q.T + kTileM - 1) / kTileM;
+        const SegPos sp = seg_pos(pos, ntiles, item + (int)gridDim.x < n_items);
+        tc::mbar_wait(b_full, it & 1);
+        tc::fence_after_sync();
+        for (int k = 0; k < ntiles; ++k, ++gt) {
+          const int p = sp.k0 + k, st = p % kStages, sl = gt % kSlots;
+          tc::mbar_wait(&sl_empty[sl], ((gt / kSlots) & 1) ^ 1);
+          tc::mbar_wait(&st_full[st], (p / kStages) & 1);
+          tc::fence_after_sync();
+          const uint32_t a = tc::smem_u32(ring + st * kStageBytes);
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+            const uint32_t bb = part ? bl : bh;
+#pragma unroll
+            for (int kk = 0; kk < kD / 16; ++kk) {
+              const uint32_t koff = (uint32_t)((kk & 3) * 32);
+              tc::mma_f16(tmem + (uint32_t)(sl * kSlotCols),
+                          tc::desc_k_sw128(a + (kk >> 2) * kTileM * 128 + koff),
+                          tc::desc_k_sw128(bb + (kk >> 2) * kBHalf + koff), idesc,
+                          (part | kk) ? 1u : 0u);
+            }
+          }
+          tc::mma_commit(&sl_full[sl]);
+        }
+        tc::mma_commit(b_empty);
+        pos = sp.next;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kCompactorFirst / 32) {
+    // ================= compactors =================
+    for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
+      const int jb = it & 1;
+      tc::mbar_wait(&job_full[jb], (it >> 1) & 1);
+      const Job job = s_job[jb];
+      char* seg = arena + g.seg_base(job.l, 0, job.h);
+      compact_rows<kD * 2, Compactors, 8>(seg, g, ctab + jb * nb_stride, ctab + jb * nb_stride,
+                                          idxbuf + jb * k_stride, job.K, job.first_moved);
+      Compactors::sync();
+      if (Compactors::tid() == 0) tc::mbar_arrive(&job_empty[jb]);
+    }
+  } else {
+    // ================= consumers =================
+    const int ct = Consumers::tid();
+    const int cw = warp - kConsumerFirst / 32;
+    const int grp = cw >> 2;                    // Y / K columns [64*grp, 64*grp + 64)
+    const int quarter = warp & 3;
+    const int trow = quarter * 32 + lane;       // TMEM lane = token row in tile
+    const float inv_sqrt_d = 1.0f / sqrtf((float)kD);
+    const float inv_2d = 1.0f / (2.0f * (float)kD);
+
+    auto release_stage = [&](int p) {
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&st_empty[p % kStages]);
+    };
+    // Sigma (fp32, two ring stages) -> B hi/lo (fp16, transposed, swizzled) + mu row
+    auto convert_sigma = [&](int p0, int item) {
+      const PressReq q = b.req[item / LH];
+      const int lh = item % LH, l = lh / g.H, h = lh % g.H;
+      const float* mu = mean_q + ((((int64_t)q.q_idx * g.L + l) * pp.num_q_heads + h) * kD);
+      for (int part = 0; part < 2; ++part) {
+        const int p = p0 + part;
+        tc::mbar_wait(&st_full[p % kStages], (p / kStages) & 1);
+        const float* sig = reinterpret_cast<const float*>(ring + (p % kStages) * kStageBytes);
+        // this stage holds Sigma rows k in [64*part, 64*part + 64): B[n][k] = Sigma[k][n]
+        for (int i = ct; i < 128 * 8; i += kThreads) {
+          const int n = i & 127, c8 = i >> 7;           // 8 chunks of 8 k's
+          const int k0 = part * 64 + c8 * 8;
+          __half hi[8], lo[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float x = sig[(c8 * 8 + e) * kD + n];
+            hi[e] = __float2half_rn(x);
+            lo[e] = __float2half_rn(x - __half2float(hi[e]));
+          }
+          *reinterpret_cast<uint4*>(bmat + b_off(n, k0)) = *reinterpret_cast<uint4*>(hi);
+          *reinterpret_cast<uint4*>(bmat + kBBytes + b_off(n, k0)) = *reinterpret_cast<uint4*>(lo);
+        }
+        release_stage(p);
+      }
+      for (int k = ct; k < kD; k += kThreads) {
+        const float x = mu[k];
+        const __half hi = __float2half_rn(x);
+        *reinterpret_cast<__half*>(bmat + b_off(128, k)) = hi;
+        *reinterpret_cast<__half*>(bmat + kBBytes + b_off(128, k)) = __float2half_rn(x - __half2float(hi));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      Consumers::sync();
+      if (ct == 0) tc::mbar_arrive(b_full);
+    };
+
+    int pos = 2, gt = 0;
+    if ((int)blockIdx.x < n_items) convert_sigma(0, blockIdx.x);
+    for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
+      const int r = item / LH, lh = item % LH, l = lh / g.H, h = lh % g.H;
+      const PressReq q = b.req[r];
+      const int T_len = q.T, K = q.K, ns = pp.n_sink;
+      const int nb = (T_len + g.bs - 1) / g.bs, ntiles = (T_len + kTileM - 1) / kTileM;
+      const bool has_next = item + (int)gridDim.x < n_items;
+      const SegPos sp = seg_pos(pos, ntiles, has_next);
+      const int jb = it & 1;
+      for (int t = ct; t < T_len; t += kThreads) zt[t] = 0.f;
+      if (ct == 0) ss.first_drop = INT_MAX;
+      Consumers::sync();
+      // ---- z_t from TMEM (Y = K.B^T) and the K rows still in SMEM ----
+      for (int k = 0; k < ntiles; ++k, ++gt) {
+        const int p = sp.k0 + k, sl = gt % kSlots;
+        tc::mbar_wait(&sl_full[sl], (gt / kSlots) & 1);
+        tc::fence_after_sync();
+        float y[32];
+        float acc = 0.f;
+        const int t = k * kTileM + trow;
+        const unsigned char* krow = ring + (p % kStages) * kStageBytes + grp * (kTileM * 128) +
+                                    (trow >> 3) * 1024 + (trow & 7) * 128;
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sl * kSlotCols + grp * 64);
+#pragma unroll
+        for (int hcol = 0; hcol < 2; ++hcol) {
+          tc::tmem_ld_32x32b_x32(taddr + (uint32_t)(hcol * 32), y);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int chunk = hcol * 4 + c;
+            const uint4 raw = *reinterpret_cast<const uint4*>(krow + ((chunk ^ (trow & 7)) << 4));
+            float kx[8];
+            unpack16<__half>(raw, kx);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc = fmaf(y[c * 8 + e], kx[e], acc);
+          }
+        }
+        float lin = 0.f;
+        if (grp == 0) {
+          float l1[16];
+          tc::tmem_ld_32x32b_x16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sl * kSlotCols + 128), l1);
+          lin = l1[0];
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
+        release_stage(p);
+        if (t < T_len) atomicAdd(&zt[t], grp == 0 ? fmaf(lin, inv_sqrt_d, acc * inv_2d) : acc * inv_2d);
+      }
+      // ---- the next segment's Sigma while the MMA warp idles on B ----
+      if (has_next) {
+        tc::mbar_wait(b_empty, it & 1);
+        convert_sigma(sp.sig_next, item + gridDim.x);
+      }
+      Consumers::sync();
+      // ---- softmax over t >= n_sink ----
+      float m = -INFINITY;
+      for (int t = ns + ct; t < T_len; t += kThreads) m = fmaxf(m, zt[t]);
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+      if (lane == 0) ss.red[cw] = m;
+      Consumers::sync();
+      m = ss.red[0];
+      for (int w = 1; w < kWarps; ++w) m = fmaxf(m, ss.red[w]);
+      float z = 0.f;
+      for (int t = ns + ct; t < T_len; t += kThreads) z += expf(zt[t] - m);
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
+      Consumers::sync();
+      if (lane == 0) ss.red[cw] = z;
+      Consumers::sync();
+      z = 0.f;
+      for (int w = 0; w < kWarps; ++w) z += ss.red[w];
+      const float inv_z = 1.0f / z;
+      // ---- V tiles: s_t = p_t * ||V_t|| (two lanes per row) ----
+      for (int k = 0; k < ntiles; ++k) {
+        const int p = sp.v0 + k;
+        tc::mbar_wait(&st_full[p % kStages], (p / kStages) & 1);
+        const int row = ct >> 1, half = ct & 1;
+        const unsigned char* vrow = ring + (p % kStages) * kStageBytes + half * (kTileM * 128) +
+                                    (row >> 3) * 1024 + (row & 7) * 128;
+        float sq = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          float vx[8];
+          unpack16<__half>(*reinterpret_cast<const uint4*>(vrow + (c << 4)), vx);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) sq = fmaf(vx[e], vx[e], sq);
+        }
+        sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+        release_stage(p);
+        const int t = k * kTileM + row;
+        if (half == 0 && t < T_len && t >= ns) zt[t] = expf(zt[t] - m) * inv_z * sqrtf(sq);
+      }
+      Consumers::sync();
+      for (int t = ct; t < ns && t < T_len; t += kThreads) zt[t] = INFINITY;
+      Consumers::sync();
+      if (out.scores) {
+        float* so = out.scores + q.score_off + (int64_t)lh * T_len;
+        for (int t = ct; t < T_len; t += kThreads) so[t] = zt[t];
+      }
+      uint32_t* keys = reinterpret_cast<uint32_t*>(zt);
+      for (int t = ct; t < T_len; t += kThreads) keys[t] = float_key(zt[t]);
+      // ---- select into the hand-off buffer ----
+      tc::mbar_wait(&job_empty[jb], ((it >> 1) & 1) ^ 1);
+      int32_t* idx = idxbuf + jb * k_stride;
+      for (int i = ct; i < nb; i += kThreads) ctab[jb * nb_stride + i] = table[(int64_t)q.slot * g.max_bpr + i];
+      Consumers::sync();
+      if (b.per_segment && q.seg0 < T_len) {
+        select_emit<Consumers>(keys, q.seg0, q.K0, idx, 0, 0, ss);
+        select_emit<Consumers>(keys + q.seg0, T_len - q.seg0, K - q.K0, idx, q.K0, q.seg0, ss);
+      } else {
+        select_emit<Consumers>(keys, T_len, K, idx, 0, 0, ss);
+      }
+      if (out.kept_idx) {
+        int32_t* ko = out.kept_idx + q.kept_off + (int64_t)lh * K;
+        for (int j = ct; j < K; j += kThreads) ko[j] = idx[j];
+      }
+      if (ct == 0) s_job[jb] = Job{l, h, K, min(ss.first_drop, K)};
+      Consumers::sync();
+      if (ct == 0) tc::mbar_arrive(&job_full[jb]);
+      pos = sp.next;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, kSlots * kSlotCols);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+bool ea_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T, int max_K) {
+  static const bool forced_simt = [] {
+    const char* e = getenv("FASTCACHE_EA_SIMT");
+    return e && e[0] == '1';
+  }();
+  if (forced_simt) return false;
+  if (dtype != FC_F16 || g.D != kD) return false;
+  if (pp.num_q_heads != g.H) return false;   // one query head per kv head
+  if (g.bs < 8 || g.bs > 128) return false;
+  return plan(g.bs, max_T, max_K).total <= 227 * 1024;
+}
+
+fc_status encode_rows(CUtensorMap* map, const void* base, int dtype, int D, uint64_t rows, int box_rows);
+
+fc_status launch_ea_tc(const Geom& g, char* arena, const int32_t* table, const PressBatch& b,
+                       const PressParams& pp, const fc_press_inputs& in, const fc_press_outputs& out,
+                       int max_K, cudaStream_t stream) {
+  CUtensorMap kmap, cmap;
+  const uint64_t rows = (uint64_t)g.L * g.num_blocks * 2 * g.H * g.bs;
+  fc_status st = encode_rows(&kmap, arena, FC_F16, g.D, rows, g.bs);
+  if (st != FC_OK) return st;
+  st = encode_rows(&cmap, in.cov_q, FC_F32, g.D, (uint64_t)b.n_total * g.L * pp.num_q_heads * g.D, 64);
+  if (st != FC_OK) return st;
+  const Smem P = plan(g.bs, b.max_T, max_K);
+  const int n_items = b.n * g.L * g.H;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = n_items < sms ? n_items : sms;
+  cudaError_t e = cudaFuncSetAttribute(ea_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P.total);
+  if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(ea_tc)");
+  ea_tc_kernel<<<grid, kEaThreads, P.total, stream>>>(arena, table, g, b, pp, kmap, cmap, in.mean_q,
+                                                     out, n_items, max_K);
+  note_launch();
+  return cuda_check(cudaGetLastError(), "ea_tc_kernel");
+}
+
+}  // namespace fc

@@ -372,18 +372,25 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-static fc_status encode_rows(CUtensorMap* map, const void* base, int dtype, int D, uint64_t rows,
-                             int box_rows) {
+// 2-D row-major tensor map [rows][D]: box = {box_cols elements, box_rows rows}.
+// 16-bit types use the 128-byte swizzle (UMMA K-major operands); fp32 is unswizzled.
+fc_status encode_rows(CUtensorMap* map, const void* base, int dtype, int D, uint64_t rows,
+                      int box_rows) {
   auto enc = get_encode();
   if (!enc) return set_error(FC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const bool f32 = dtype == FC_F32;
+  const int esz = f32 ? 4 : 2;
   const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)D * 2};
-  const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)D * esz};
+  const cuuint32_t box[2] = {f32 ? (cuuint32_t)D : 64u, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, dtype == FC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                   2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUtensorMapDataType dt = f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                     : (dtype == FC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+  CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   f32 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(FC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return FC_OK;
 }

@@ -44,9 +44,9 @@ def _model(dtype, L, H, D):
     return ModelConfig("m", L, H, D, 4 if dtype == "float32" else 2)
 
 
-def _make_pool(cuda, cfg, dtype, mode=PoolMode.POOLED, cap_tokens=1 << 16, **kw):
+def _make_pool(cuda, cfg, dtype, mode=PoolMode.POOLED, cap_tokens=1 << 16, max_tokens=8192, **kw):
     return KVCachePool(cfg, cap_tokens * cfg.bytes_per_token, mode, device=cuda, kv_dtype=dtype,
-                       max_handles=64, max_tokens_per_handle=4096, **kw)
+                       max_handles=64, max_tokens_per_handle=max_tokens, **kw)
 
 
 def _ledger_twin(cfg, cap_tokens, mode):
@@ -249,7 +249,8 @@ def test_snapkv_parity(cuda, dtype, L, H, gq, D, specs, w, p):
 
 
 @pytest.mark.parametrize("dtype,L,H,gq,D,specs,ns", [
-    ("float16", 2, 2, 1, 128, [(576, 200), (0, 1024)], 4),
+    ("float16", 2, 2, 1, 128, [(576, 200), (0, 1024)], 4),               # tcgen05 path
+    ("float16", 1, 2, 1, 128, [(576, 7616), (1, 1500), (0, 5), (130, 0)], 4),   # tcgen05, T=8192
     ("bfloat16", 1, 2, 2, 64, [(0, 300)], 4),
     ("float32", 1, 1, 2, 128, [(30, 40)], 2),
 ])
