@@ -196,6 +196,19 @@ def traffic_from_profile(config: str):
         return None
 
 
+def _allreduce(value: float, op: str, device) -> float:
+    """Max/sum over ranks (NCCL on the GPU tensor, gloo on a CPU copy)."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return value
+    dev = device if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def run_serving_bench(args, rank, world, local_rank):
     """Config 5: route the trace (NCCL occupancy all-gather), serve it with real compression."""
     import torch
@@ -219,12 +232,10 @@ def run_serving_bench(args, rank, world, local_rank):
             runs.append(st)
     my_ms = sum(sum(r.compress_ms) for r in runs)
     my_tok = sum(r.compressed_tokens for r in runs)
-    t = torch.tensor([my_ms], dtype=torch.float64, device=device)
-    tok = torch.tensor([my_tok], dtype=torch.float64, device=device)
+    max_ms = _allreduce(my_ms, "max", device)
+    all_tok = _allreduce(float(my_tok), "sum", device)
     ttft = runs[-1].ttft
     if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(tok, op=torch.distributed.ReduceOp.SUM)
         gathered = [None] * world
         torch.distributed.all_gather_object(gathered, ttft)
         ttft = [x for part in gathered for x in part]
@@ -232,9 +243,9 @@ def run_serving_bench(args, rank, world, local_rank):
 
     summ = runs[-1].summary()
     return {
-        "metric": "compressed KV tokens/s", "value": float(tok.item()) / (float(t.item()) / 1e3),
+        "metric": "compressed KV tokens/s", "value": all_tok / (max_ms / 1e3),
         "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": float(t.item()) / args.steps, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f16", "data": "synthetic trace (serving.make_trace, seed 0)",
         "config": {"workload": f"c5: {CONFIGS['c5']}", "requests": 2000, "rate_rps": 40.0,
                    "pool_capacity_bytes_per_gpu": capacity,
@@ -283,11 +294,9 @@ def run_churn_bench(args, rank, world, local_rank):
                                         max_wave=max_wave))
     torch.cuda.synchronize(device)
     my_ms = sum(r.total_compress_ms for r in runs)
-    t = torch.tensor([my_ms], dtype=torch.float64, device=device)
     if world > 1:
         torch.distributed.barrier()
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = _allreduce(my_ms, "max", device)
     peak, peak_kind = measured_peak()
     abytes = alg_bytes(cfg, specs, comp)
     achieved = abytes * args.steps / (my_ms / 1e3) / 1e9
@@ -372,10 +381,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         torch.distributed.barrier()
     total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=device)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = _allreduce(total_ms, "max", device)
     value = job_tokens * args.steps / (max_ms / 1e3)
     abytes = alg_bytes(cfg, specs, comp)
     peak, peak_kind = measured_peak()
@@ -460,13 +466,11 @@ def run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world, job_t
             times.append(ev0.elapsed_time(ev1))
             d2h = kept_host.numel() * kept_host.element_size()
         pool.release_batch(hs, 2.0)
-    t = torch.tensor([sum(times)], dtype=torch.float64, device=device)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    max_ms = _allreduce(sum(times), "max", device)
     tokens = job_tokens * len(times)
-    return {"value": tokens / (float(t.item()) / 1e3), "unit": "tokens/s",
+    return {"value": tokens / (max_ms / 1e3), "unit": "tokens/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": float(t.item()) / len(times),
+            "ms_per_step": max_ms / len(times),
             "path": "pinned host KV -> H2D -> store_tokens (ingest kernel) -> compress_batch -> "
                     "kept indices D2H"}
 
@@ -559,9 +563,16 @@ def main():
         return
     import torch
 
+    # FASTCACHE_DIST_BACKEND=gloo lets several ranks share one GPU (multi-rank path tests on
+    # a single-GPU box); the default is one rank per GPU over NCCL.
+    backend = os.environ.get("FASTCACHE_DIST_BACKEND", "nccl")
+    local_rank = local_rank % max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            torch.distributed.init_process_group(backend)
     if args.config == "c4":
         result = run_churn_bench(args, rank, world, local_rank)
     elif args.config == "c5":

@@ -70,11 +70,13 @@ class OccupancyExchange:
         import torch
         import torch.distributed as dist
 
-        mine = torch.tensor([free_bytes, queued_raw, inflight, backlog_tokens], dtype=torch.int64,
-                            device=self.device)
         if not dist.is_available() or not dist.is_initialized():
-            return [mine.tolist()]
+            return [[free_bytes, queued_raw, inflight, backlog_tokens]]
+        # NCCL moves device tensors; gloo (CPU tests) moves host tensors
+        dev = self.device if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+        mine = torch.tensor([free_bytes, queued_raw, inflight, backlog_tokens], dtype=torch.int64,
+                            device=dev)
         world = dist.get_world_size(self.group)
-        out = torch.empty(world * 4, dtype=torch.int64, device=self.device)
+        out = torch.empty(world * 4, dtype=torch.int64, device=dev)
         dist.all_gather_into_tensor(out, mine, group=self.group)
         return out.view(world, 4).tolist()
