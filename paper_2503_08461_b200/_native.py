@@ -11,7 +11,9 @@ from __future__ import annotations
 import ctypes
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libfastcache.so")
+LIB_PATH = os.environ.get(
+    "FASTCACHE_LIB",
+    os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libfastcache.so"))
 
 # fc_status
 OK = 0

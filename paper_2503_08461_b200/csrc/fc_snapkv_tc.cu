@@ -35,7 +35,22 @@
 
 namespace fc {
 
-constexpr int kTcStages = 4;
+#ifdef FC_TRACE
+// Debug build only (make trace): per-CTA, per-segment %globaltimer stamps.
+__device__ unsigned long long g_fc_trace[148 * 64 * 8];
+__device__ __forceinline__ void trace_stamp(int it, int slot) {
+  if (it < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_fc_trace[(blockIdx.x * 64 + it) * 8 + slot] = t;
+  }
+}
+#define FC_STAMP(it, slot) trace_stamp(it, slot)
+#else
+#define FC_STAMP(it, slot) ((void)0)
+#endif
+
+constexpr int kTcStages = 3;
 constexpr int kTileM = 128;
 constexpr int kSlots = 16;                      // TMEM ring: 16 x 32 fp32 columns
 constexpr int kWin = 32;                        // window queries (UMMA N)
@@ -150,6 +165,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const int st = gtile % kTcStages;
           tc::mbar_wait(&st_empty[st], ((gtile / kTcStages) & 1) ^ 1);
           const int n_chunks = min(chunks, nb - k * chunks);
+          if (k == 0) FC_STAMP(it, 0);
+          if (k == ntiles - 1) FC_STAMP(it, 1);
           tc::mbar_expect_tx(&st_full[st], (uint32_t)(n_chunks * g.bs * D * 2));
           unsigned char* dst = stages + st * plan.tile_bytes;
           for (int c = 0; c < n_chunks; ++c) {
@@ -192,6 +209,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           tc::mma_commit(&sl_full[sl]);
         }
         tc::mma_commit(&q_empty[qb]);
+        FC_STAMP(it, 2);
       }
     }
     __syncwarp();
@@ -200,13 +218,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
       const int jb = it & 1;
       tc::mbar_wait(&job_full[jb], (it >> 1) & 1);
+      if (Compactors::tid() == 0) FC_STAMP(it, 6);
       const CompactJob job = s_job[jb];
       char* seg = arena + g.seg_base(job.l, 0, job.h);
       compact_rows<D * (int)sizeof(T), Compactors, 8>(seg, g, ctab + jb * nb_stride,
                                                    ctab + jb * nb_stride, idxbuf + jb * t_stride,
                                                    job.K, job.first_moved);
       Compactors::sync();
-      if (Compactors::tid() == 0) tc::mbar_arrive(&job_empty[jb]);
+      if (Compactors::tid() == 0) {
+        FC_STAMP(it, 7);
+        tc::mbar_arrive(&job_empty[jb]);
+      }
     }
   } else {
     // ================= consumers (8 warps, named barrier 1) =================
@@ -243,6 +265,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int j = 0; j < 16; ++j)
           if (t < T_len && t <= T_len - kWin + grp * 16 + j) acc[j] = fmaxf(acc[j], v[j] * scale);
       }
+      if (ct == 0) FC_STAMP(it, 3);
 #pragma unroll
       for (int j = 0; j < 16; ++j)
 #pragma unroll
@@ -309,6 +332,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
       gtile += ntiles;
+      if (ct == 0) FC_STAMP(it, 4);
       Consumers::sync();
       // avg-pool (zero pad, count_include_pad), forced window
       const int half = pp.pool_kernel / 2;
@@ -348,7 +372,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       if (ct == 0) s_job[jb] = CompactJob{l, h, K, min(ss.first_drop, K)};
       Consumers::sync();  // idx, ctab, job complete; sc / ss reused by the next segment
-      if (ct == 0) tc::mbar_arrive(&job_full[jb]);
+      if (ct == 0) {
+        FC_STAMP(it, 5);
+        tc::mbar_arrive(&job_full[jb]);
+      }
     }
   }
   tc::fence_before_sync();
@@ -441,3 +468,9 @@ fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t*
 }
 
 }  // namespace fc
+
+#ifdef FC_TRACE
+extern "C" FC_API fc_status fc_debug_trace_read(void* host, uint64_t bytes) {
+  return fc::cuda_check(cudaMemcpyFromSymbol(host, fc::g_fc_trace, bytes), "trace read");
+}
+#endif

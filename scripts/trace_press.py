@@ -1,0 +1,48 @@
+#!/usr/bin/env python
+"""Per-role timelines of the warp-specialised SnapKV kernel (debug build).
+
+    make -C paper_2503_08461_b200/csrc trace
+    FASTCACHE_LIB=paper_2503_08461_b200/_lib/libfastcache_trace.so python scripts/trace_press.py
+"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2503_08461_b200 import KVCachePool, _native, kv_bytes  # noqa: E402
+
+cfg, dtype, specs, comp = bench.workload(sys.argv[1] if len(sys.argv) > 1 else "c3")
+dev = torch.device("cuda", 0)
+pool = KVCachePool(cfg, sum(kv_bytes(cfg, s.total_tokens) for s in specs), device=dev,
+                   kv_dtype=dtype, max_handles=256, max_tokens_per_handle=4096)
+ins = bench.press_inputs(comp, cfg, len(specs), dev, torch, seed=1)
+for rep in range(3):
+    hs = pool.allocate_batch(list(range(len(specs))), specs, 0.0)
+    pool.synth_fill(hs, seed=1)
+    torch.cuda.synchronize()
+    pool.compress_batch(hs, comp, 1.0, **ins)
+    torch.cuda.synchronize()
+    pool.release_batch(hs, 2.0)
+buf = np.zeros(148 * 64 * 8, dtype=np.uint64)
+lib = _native.load()
+lib.fc_debug_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
+assert lib.fc_debug_trace_read(buf.ctypes.data, buf.nbytes) == 0
+tr = buf.reshape(148, 64, 8).astype(np.int64)
+t0 = tr[tr > 0].min()
+names = ["prod_first", "prod_last", "mma_done", "cons_p1", "cons_p3", "cons_sel", "comp_start", "comp_end"]
+for cta in (0, 77):
+    print(f"CTA {cta} (us from kernel start)")
+    for it in range(0, 12):
+        row = (tr[cta, it] - t0) / 1e3
+        print(f"  seg {it:2d} " + " ".join(f"{n}={v:8.1f}" for n, v in zip(names, row)))
+# steady-state per-segment durations averaged over CTAs and segments 4..40
+d = (tr[:, 4:40] - t0) / 1e3
+seg_period = np.diff(d[:, :, 5], axis=1).mean()
+print("mean segment period (consumer handoff to handoff): %.2f us" % seg_period)
+print("mean consumer p1-wait->p3 %.2f, p3->select %.2f us" % ((d[:, :, 4] - d[:, :, 3]).mean(), (d[:, :, 5] - d[:, :, 4]).mean()))
+print("mean compactor busy %.2f us, period %.2f us" % ((d[:, :, 7] - d[:, :, 6]).mean(), np.diff(d[:, :, 6], axis=1).mean()))
+print("mean producer first->last K tile %.2f us" % (d[:, :, 1] - d[:, :, 0]).mean())
