@@ -26,9 +26,12 @@ struct NamedGroup {
   }
 };
 
+constexpr int kRadixBins = 256;  // 8-bit digits, 4 passes
+
 struct SelectScratch {
-  uint32_t hist[256];
+  uint32_t hist[kRadixBins];
   int32_t warp_tot[kWarps];
+  uint32_t emit_tot[2][kWarps];   // double-buffered packed (gt | eq << 16) warp counts
   int32_t sel_bin;
   int32_t sel_krem;
   int32_t first_drop;
@@ -56,82 +59,108 @@ __device__ __forceinline__ int block_excl_scan(bool pred, int32_t* warp_tot, int
 }
 
 // Top-K of keys[0..n) by (key desc, index asc); writes idx_base + i of the kept
-// i, ascending, to out[out_base ...]. `out` may alias `keys` (write positions
-// never pass unread keys: out_base <= keys' own offset and each write index is
-// <= its source index).
+// i, ascending, to out[out_base ...]; lowers s.first_drop to the first dropped
+// idx_base + i. `out` may alias `keys`: kept element i lands at
+// G(i) + min(E(i), need) <= i (G/E = greater/equal-to-threshold keys before i).
+//
+// Threshold: 4-pass radix select on 8-bit digits (one warp scans 8 bins per
+// lane; the next pass's histogram reset rides behind the scan's barrier).
+// Emission: one ballot scan per 256-key tile carrying both the > tau and == tau
+// counts, double-buffered so each tile costs a single barrier.
 template <class G = CtaGroup>
 __device__ void select_emit(const uint32_t* keys, int n, int K, int32_t* out, int out_base,
                             int idx_base, SelectScratch& s) {
-  uint32_t tau = 0;
-  int need = 0;
-  const bool all = K >= n;
-  if (!all) {
-    uint32_t prefix = 0, mask = 0;
-    int krem = K;
-    for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int i = G::tid(); i < 256; i += kThreads) s.hist[i] = 0;
-      G::sync();
-      for (int i = G::tid(); i < n; i += kThreads) {
+  const int tid = G::tid(), lane = threadIdx.x & 31, warp = tid >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  if (K >= n) {
+    for (int i = tid; i < n; i += kThreads) out[out_base + i] = idx_base + i;
+    G::sync();
+    return;
+  }
+  uint32_t prefix = 0, mask = 0;
+  int krem = K;
+#pragma unroll 1
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    for (int i = tid; i < kRadixBins; i += kThreads) s.hist[i] = 0;
+    G::sync();
+    for (int base = 0; base < n; base += kThreads) {
+      const int i = base + tid;
+      if (i < n) {
         const uint32_t k = keys[i];
         if ((k & mask) == prefix) atomicAdd(&s.hist[(k >> shift) & 255u], 1u);
       }
-      G::sync();
-      if (G::tid() < 32) {
-        const int lane = G::tid();
-        uint32_t c[8];
-        uint32_t local = 0;
+    }
+    G::sync();
+    if (tid < 32) {
+      constexpr int per = kRadixBins / 32;  // 8 bins per lane, lane 31 owns the top
+      uint32_t c[per];
+      uint32_t local = 0;
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          c[b] = s.hist[lane * 8 + b];
-          local += c[b];
-        }
-        uint32_t incl = local;  // sum over lanes >= lane
+      for (int b = 0; b < per; ++b) {
+        c[b] = s.hist[lane * per + b];
+        local += c[b];
+      }
+      uint32_t incl = local;  // sum over lanes >= lane
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const uint32_t y = __shfl_down_sync(0xffffffffu, incl, off);
-          if (lane + off < 32) incl += y;
-        }
-        const uint32_t above = incl - local;
-        if (above < (uint32_t)krem && (uint32_t)krem <= incl) {
-          uint32_t cum = above;
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_down_sync(0xffffffffu, incl, off);
+        if (lane + off < 32) incl += y;
+      }
+      const uint32_t above = incl - local;
+      if (above < (uint32_t)krem && (uint32_t)krem <= incl) {
+        uint32_t cum = above;
 #pragma unroll
-          for (int b = 7; b >= 0; --b) {
-            if (cum + c[b] >= (uint32_t)krem) {
-              s.sel_bin = lane * 8 + b;
-              s.sel_krem = krem - (int)cum;
-              break;
-            }
-            cum += c[b];
+        for (int b = per - 1; b >= 0; --b) {
+          if (cum + c[b] >= (uint32_t)krem) {
+            s.sel_bin = lane * per + b;
+            s.sel_krem = krem - (int)cum;
+            break;
           }
+          cum += c[b];
         }
       }
-      G::sync();
-      prefix |= (uint32_t)s.sel_bin << shift;
-      mask |= 255u << shift;
-      krem = s.sel_krem;
-      G::sync();
     }
-    tau = prefix;
-    need = krem;
+    G::sync();
+    prefix |= (uint32_t)s.sel_bin << shift;
+    mask |= 255u << shift;
+    krem = s.sel_krem;
   }
-  int running = 0, running_eq = 0;
-  for (int base = 0; base < n; base += kThreads) {
-    const int i = base + G::tid();
+  const uint32_t tau = prefix;
+  const int need = krem;
+  int run_gt = 0, run_eq = 0, buf = 0;
+  bool drop_found = false;
+  for (int base = 0; base < n; base += kThreads, buf ^= 1) {
+    const int i = base + tid;
     const bool valid = i < n;
     const uint32_t k = valid ? keys[i] : 0u;
-    bool kept = valid;
-    if (!all) {
-      const bool eq = valid && k == tau;
-      int eq_total;
-      const int eq_pre = block_excl_scan<G>(eq, s.warp_tot, eq_total);
-      kept = valid && (k > tau || (eq && running_eq + eq_pre < need));
-      running_eq += eq_total;
+    const bool gt = valid && k > tau, eq = valid && k == tau;
+    const unsigned bg = __ballot_sync(0xffffffffu, gt), be = __ballot_sync(0xffffffffu, eq);
+    if (lane == 0) s.emit_tot[buf][warp] = (uint32_t)__popc(bg) | ((uint32_t)__popc(be) << 16);
+    G::sync();
+    int g_before = 0, e_before = 0, g_tot = 0, e_tot = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = s.emit_tot[buf][w];
+      const int cg = (int)(c & 0xFFFFu), ce = (int)(c >> 16);
+      g_before += w < warp ? cg : 0;
+      e_before += w < warp ? ce : 0;
+      g_tot += cg;
+      e_tot += ce;
     }
-    int tot;
-    const int pre = block_excl_scan<G>(kept, s.warp_tot, tot);
-    if (kept) out[out_base + running + pre] = idx_base + i;
-    if (valid && !kept) atomicMin(&s.first_drop, idx_base + i);
-    running += tot;
+    const int G_i = run_gt + g_before + __popc(bg & lt_mask);
+    const int E_i = run_eq + e_before + __popc(be & lt_mask);
+    const bool kept = gt || (eq && E_i < need);
+    if (kept) out[out_base + G_i + min(E_i, need)] = idx_base + i;
+    if (!drop_found) {
+      const unsigned dropped = __ballot_sync(0xffffffffu, valid && !kept);
+      if (dropped) {
+        if (lane == 0) atomicMin(&s.first_drop, idx_base + base + warp * 32 + __ffs(dropped) - 1);
+        drop_found = true;  // later tiles only hold larger indices
+      }
+    }
+    run_gt += g_tot;
+    run_eq += e_tot;
   }
   G::sync();
 }

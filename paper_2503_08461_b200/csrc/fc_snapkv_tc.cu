@@ -37,12 +37,12 @@ namespace fc {
 
 #ifdef FC_TRACE
 // Debug build only (make trace): per-CTA, per-segment %globaltimer stamps.
-__device__ unsigned long long g_fc_trace[148 * 64 * 8];
+__device__ unsigned long long g_fc_trace[148 * 64 * 16];
 __device__ __forceinline__ void trace_stamp(int it, int slot) {
   if (it < 64) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_fc_trace[(blockIdx.x * 64 + it) * 8 + slot] = t;
+    g_fc_trace[(blockIdx.x * 64 + it) * 16 + slot] = t;
   }
 }
 #define FC_STAMP(it, slot) trace_stamp(it, slot)
@@ -221,9 +221,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (Compactors::tid() == 0) FC_STAMP(it, 6);
       const CompactJob job = s_job[jb];
       char* seg = arena + g.seg_base(job.l, 0, job.h);
+#ifndef FC_NO_COMPACT
       compact_rows<D * (int)sizeof(T), Compactors, 8>(seg, g, ctab + jb * nb_stride,
                                                    ctab + jb * nb_stride, idxbuf + jb * t_stride,
                                                    job.K, job.first_moved);
+#endif
       Compactors::sync();
       if (Compactors::tid() == 0) {
         FC_STAMP(it, 7);
@@ -284,6 +286,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       float mj[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) mj[j] = s_m[grp * 16 + j];
+      if (ct == 0) FC_STAMP(it, 8);
       // pass 2: per-query sum of exp
 #pragma unroll
       for (int j = 0; j < 16; ++j) acc[j] = 0.f;
@@ -293,9 +296,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
         const int t = k * kTileM + row;
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (t < T_len && t <= T_len - kWin + grp * 16 + j) acc[j] += tc::ex2(fmaf(v[j], scale, -mj[j]));
+        for (int j = 0; j < 16; ++j) {
+          const float e = (t < T_len && t <= T_len - kWin + grp * 16 + j) ? tc::ex2(fmaf(v[j], scale, -mj[j])) : 0.f;
+          acc[j] += e;
+          v[j] = e;
+        }
+        tc::tmem_st_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);   // exps replace the logits
       }
+      tc::tmem_store_wait();
+      if (ct == 0) FC_STAMP(it, 9);
 #pragma unroll
       for (int j = 0; j < 16; ++j)
 #pragma unroll
@@ -314,6 +323,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       float zj[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) zj[j] = s_zinv[grp * 16 + j];
+      if (ct == 0) FC_STAMP(it, 10);
       // pass 3: partial window mean of the normalised probabilities; frees TMEM slots
       for (int k = 0; k < ntiles; ++k) {
         const int sl = (gtile + k) % kSlots;
@@ -326,9 +336,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (t < n_keep) {
           float s = 0.f;
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (t <= T_len - kWin + grp * 16 + j) s += tc::ex2(fmaf(v[j], scale, -mj[j])) * zj[j];
-          s1[grp * s1_stride + t] = s;
+          for (int j = 0; j < 16; ++j) s = fmaf(v[j], zj[j], s);   // masked entries are 0
+          s1[grp * s1_stride + t] = s * (1.0f / (float)kWin);
         }
       }
       gtile += ntiles;
@@ -336,15 +345,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       Consumers::sync();
       // avg-pool (zero pad, count_include_pad), forced window
       const int half = pp.pool_kernel / 2;
+      const float inv_p = 1.0f / (float)pp.pool_kernel;
       for (int t = ct; t < T_len; t += kThreads) {
         float v = INFINITY;
         if (t < n_keep) {
           float a = 0.f;
-          for (int o = -half; o <= half; ++o) {
-            const int u = t + o;
-            a += (u >= 0 && u < n_keep) ? (s1[u] + s1[s1_stride + u]) / (float)kWin : 0.f;
-          }
-          v = a / (float)pp.pool_kernel;
+          const int u0 = max(0, t - half), u1 = min(n_keep - 1, t + half);
+          for (int u = u0; u <= u1; ++u) a += s1[u] + s1[s1_stride + u];
+          v = a * inv_p;
         }
         sc[t] = v;
       }
@@ -356,6 +364,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       uint32_t* keys = reinterpret_cast<uint32_t*>(sc);
       for (int t = ct; t < T_len; t += kThreads) keys[t] = float_key(sc[t]);
       Consumers::sync();
+      if (ct == 0) FC_STAMP(it, 12);
       // hand the kept list to the compactors (double-buffered)
       tc::mbar_wait(&job_empty[jb], ((it >> 1) & 1) ^ 1);
       int32_t* idx = idxbuf + jb * t_stride;

@@ -27,17 +27,17 @@ for rep in range(3):
     pool.compress_batch(hs, comp, 1.0, **ins)
     torch.cuda.synchronize()
     pool.release_batch(hs, 2.0)
-buf = np.zeros(148 * 64 * 8, dtype=np.uint64)
+buf = np.zeros(148 * 64 * 16, dtype=np.uint64)
 lib = _native.load()
 lib.fc_debug_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
 assert lib.fc_debug_trace_read(buf.ctypes.data, buf.nbytes) == 0
-tr = buf.reshape(148, 64, 8).astype(np.int64)
+tr = buf.reshape(148, 64, 16).astype(np.int64)
 t0 = tr[tr > 0].min()
 names = ["prod_first", "prod_last", "mma_done", "cons_p1", "cons_p3", "cons_sel", "comp_start", "comp_end"]
 for cta in (0, 77):
     print(f"CTA {cta} (us from kernel start)")
     for it in range(0, 12):
-        row = (tr[cta, it] - t0) / 1e3
+        row = (tr[cta, it, :8] - t0) / 1e3
         print(f"  seg {it:2d} " + " ".join(f"{n}={v:8.1f}" for n, v in zip(names, row)))
 # steady-state per-segment durations averaged over CTAs and segments 4..40
 d = (tr[:, 4:40] - t0) / 1e3
@@ -46,3 +46,11 @@ print("mean segment period (consumer handoff to handoff): %.2f us" % seg_period)
 print("mean consumer p1-wait->p3 %.2f, p3->select %.2f us" % ((d[:, :, 4] - d[:, :, 3]).mean(), (d[:, :, 5] - d[:, :, 4]).mean()))
 print("mean compactor busy %.2f us, period %.2f us" % ((d[:, :, 7] - d[:, :, 6]).mean(), np.diff(d[:, :, 6], axis=1).mean()))
 print("mean producer first->last K tile %.2f us" % (d[:, :, 1] - d[:, :, 0]).mean())
+if len(sys.argv) > 2 and sys.argv[2] == "sub":
+    print("sub: p1->red1 %.2f  red1->pass2 %.2f  pass2->red2 %.2f  red2->p3 %.2f  p3->keys %.2f  keys->sel %.2f us" % (
+        (d[:, :, 8] - d[:, :, 3]).mean(), (d[:, :, 9] - d[:, :, 8]).mean(), (d[:, :, 10] - d[:, :, 9]).mean(),
+        (d[:, :, 4] - d[:, :, 10]).mean(), (d[:, :, 12] - d[:, :, 4]).mean(), (d[:, :, 5] - d[:, :, 12]).mean()))
+if len(sys.argv) > 2 and sys.argv[2] == "fine":
+    print("fine: p3->pool %.2f  pool->keys %.2f  keys->ctab %.2f  ctab->handoff %.2f us" % (
+        (d[:, :, 0] - d[:, :, 4]).mean(), (d[:, :, 1] - d[:, :, 0]).mean(),
+        (d[:, :, 2] - d[:, :, 1]).mean(), (d[:, :, 5] - d[:, :, 2]).mean()))
