@@ -196,6 +196,19 @@ struct Compactor {
       }
     }
   }
+  // Pull the source rows (K and V) of ranks [j0, j0 + kChunk) towards L2 so the
+  // later register loads hit L2: one bulk prefetch per row, no registers held.
+  __device__ __forceinline__ void prefetch(int j0) const {
+    for (int r = G::tid(); r < 2 * kChunk; r += kThreads) {
+      const int kv = r >= kChunk, j = j0 + (kv ? r - kChunk : r);
+      if (j < K) {
+        const int src = idx[j];
+        const char* p = seg + kv * kv_off + (int64_t)s_src[src >> g.bs_shift] * g.block_stride +
+                        (int64_t)(src & (g.bs - 1)) * kRowBytes;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "n"(kRowBytes) : "memory");
+      }
+    }
+  }
   __device__ __forceinline__ void store(int j0, const uint4 (&buf)[kItems]) const {
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
@@ -216,7 +229,10 @@ struct Compactor {
 // place because idx is ascending (idx[j] >= j): chunk c writes ranks
 // [cW, (c+1)W) while chunk c+1 only reads positions >= (c+1)W, and the barrier
 // before chunk c+1's stores orders them after every read of chunks <= c+1.
-template <int kRowBytes, class G = CtaGroup, int kItems = 4>
+#ifndef FC_PF
+#define FC_PF 2
+#endif
+template <int kRowBytes, class G = CtaGroup, int kItems = 4, int kPrefetch = FC_PF>
 __device__ __forceinline__ void compact_rows(char* __restrict__ seg, const Geom& g,
                                              const int32_t* s_src, const int32_t* s_dst,
                                              const int32_t* idx, int K, int j_start) {
@@ -225,15 +241,19 @@ __device__ __forceinline__ void compact_rows(char* __restrict__ seg, const Geom&
   if (j_start >= K) return;
   uint4 a[kItems], b[kItems];
   int j0 = j_start;
+#pragma unroll
+  for (int d = 1; d <= kPrefetch; ++d) c.prefetch(j0 + d * C::kChunk);
   c.load(j0, a);
   G::sync();
   while (true) {
     const int j1 = j0 + C::kChunk;
+    if (kPrefetch > 0) c.prefetch(j1 + kPrefetch * C::kChunk);
     if (j1 < K) c.load(j1, b);
     c.store(j0, a);
     if (j1 >= K) break;
     G::sync();
     const int j2 = j1 + C::kChunk;
+    if (kPrefetch > 0) c.prefetch(j2 + kPrefetch * C::kChunk);
     if (j2 < K) c.load(j2, a);
     c.store(j1, b);
     if (j2 >= K) break;
