@@ -46,7 +46,20 @@ __device__ __forceinline__ void score_knorm(const char* __restrict__ seg, const 
   // like fadd(fmul(x, x), acc) (the oracle's order) with half the instructions.
   constexpr bool kExactSquare = sizeof(T) == 2;
   const int lr = threadIdx.x % kLPR, rp = threadIdx.x / kLPR;
+  // bulk L2 prefetch of whole block chunks (bs rows each) kPfIters iterations ahead
+  constexpr int kPfIters = 2;
+  const int chunk_bytes = g.bs * kRowBytes;
+  auto prefetch_rows = [&](int r0, int r1) {
+    for (int c = (r0 >> g.bs_shift) + threadIdx.x; c < ((min(r1, T_len) + g.bs - 1) >> g.bs_shift);
+         c += kThreads)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                       seg + (int64_t)s_tab[c] * g.block_stride),
+                   "r"(chunk_bytes)
+                   : "memory");
+  };
+  prefetch_rows(0, kPfIters * kRPP * kU);
   for (int t0 = 0; t0 < T_len; t0 += kRPP * kU) {
+    prefetch_rows(t0 + kPfIters * kRPP * kU, t0 + (kPfIters + 1) * kRPP * kU);
     uint4 v[kU][kVPL];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
