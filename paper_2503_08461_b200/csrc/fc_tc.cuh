@@ -5,6 +5,7 @@
 
 #include <cuda.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace fc {
 namespace tc {
@@ -25,6 +26,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+#ifndef FC_WATCHDOG
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -34,6 +36,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+#else
+// Debug build: bounded wait that reports the stuck barrier and traps.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  for (long long spin = 0;; ++spin) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (ok) return;
+    if (spin == (1ll << 22)) {
+      printf("FC_WATCHDOG cta %d warp %d lane %d bar_smem 0x%x phase %u\n", (int)blockIdx.x,
+             (int)(threadIdx.x >> 5), (int)(threadIdx.x & 31), smem_u32(bar), phase);
+    }
+    if (spin == (1ll << 23)) asm volatile("trap;");
+  }
+}
+#endif
 
 // ---- TMA --------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
