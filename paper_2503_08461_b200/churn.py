@@ -17,8 +17,8 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Callable, Sequence
 
-from .kv import CompressorSpec, KVCacheSpec, kv_bytes
-from .pool import CacheHandle, KVCachePool
+from .kv import CompressorSpec, KVCacheSpec, compressed_spec, kv_bytes
+from .pool import CacheHandle, KVCachePool, PoolMode
 
 
 @dataclass
@@ -69,6 +69,10 @@ def run_waves(pool: KVCachePool, specs: Sequence[KVCacheSpec], comp: CompressorS
         wave = []
         for i in pending:
             need = kv_bytes(pool.config, specs[i].total_tokens)
+            if pool.mode is PoolMode.LEGACY_ZOMBIE:
+                # legacy keeps the raw cache next to its compressed copy: reserve both
+                # (the reference engine's COMPRESS estimate, engine.py:380-385)
+                need += kv_bytes(pool.config, compressed_spec(specs[i], comp).total_tokens)
             if need > avail or len(wave) == max_wave:
                 break
             wave.append(i)
