@@ -428,8 +428,12 @@ def run_ours(args, rank, world, local_rank):
 
 
 def run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world, job_tokens):
-    """Same metric through the public API with host buffers: H2D raw KV + compress + D2H kept."""
+    """Same metric through the public API with host buffers: every step hands the pool the
+    batch's raw KV in pinned host memory (``compress_batch(host_kv=...)``) plus the press
+    inputs (H2D), and reads the kept indices back (D2H)."""
     import torch
+
+    from paper_2503_08461_b200 import PoolMode, PressKind
 
     stream = torch.cuda.current_stream(device)
     n = len(specs)
@@ -443,8 +447,11 @@ def run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world, job_t
         buf.copy_(pool.load_tokens(h))
         host.append(buf)
     pool.release_batch(hs, 0.0)
-    staging = [torch.empty(shp, dtype=tdt, device=device) for shp in shapes]
-    h2d = sum(b.numel() * b.element_size() for b in host)
+    host_ins = {k: v.cpu().pin_memory() for k, v in ins.items()}
+    dev_ins = {k: torch.empty_like(v) for k, v in ins.items()}
+    split = pool.mode is PoolMode.POOLED and comp.press in (PressKind.KNORM, PressKind.SNAPKV)
+    raw_bytes = sum(b.numel() * b.element_size() for b in host)
+    kept_tokens = None
     kept_host = None
     times, d2h = [], 0
     for step in range(args.warmup + args.e2e_steps):
@@ -452,10 +459,9 @@ def run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world, job_t
         torch.cuda.synchronize(device)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        for h, st, hb in zip(hs, staging, host):
-            st.copy_(hb, non_blocking=True)
-            pool.store_tokens(h, st)
-        res = pool.compress_batch(hs, comp, 1.0, return_indices=True, **ins)
+        for k, v in host_ins.items():
+            dev_ins[k].copy_(v, non_blocking=True)
+        res = pool.compress_batch(hs, comp, 1.0, return_indices=True, host_kv=host, **dev_ins)
         flat = torch.cat([k.reshape(-1) for k in res.kept_idx])
         if kept_host is None:
             kept_host = torch.empty(flat.shape, dtype=flat.dtype, pin_memory=True)
@@ -465,14 +471,21 @@ def run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world, job_t
         if step >= args.warmup:
             times.append(ev0.elapsed_time(ev1))
             d2h = kept_host.numel() * kept_host.element_size()
+        kept_tokens = sum(h.spec.total_tokens for h in hs)
         pool.release_batch(hs, 2.0)
     max_ms = _allreduce(sum(times), "max", device)
     tokens = job_tokens * len(times)
+    bpt = cfg.bytes_per_token
+    kv_h2d = (raw_bytes // 2 + kept_tokens * bpt // 2) if split else raw_bytes
+    h2d = kv_h2d + sum(v.numel() * v.element_size() for v in host_ins.values())
     return {"value": tokens / (max_ms / 1e3), "unit": "tokens/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": max_ms / len(times),
-            "path": "pinned host KV -> H2D -> store_tokens (ingest kernel) -> compress_batch -> "
-                    "kept indices D2H"}
+            "pcie_gbs": (h2d + d2h) / (max_ms / len(times) / 1e3) / 1e9,
+            "path": ("pinned host KV -> compress_batch(host_kv=...): " +
+                     ("K planes DMA (double-buffered staging) -> score/select/compact -> kept V "
+                      "rows zero-copy from host" if split else "K+V DMA -> compress") +
+                     "; press inputs H2D; kept indices D2H")}
 
 
 def cpu_reference(args, cfg, dtype, specs, comp, reps: int | None = None):

@@ -16,6 +16,8 @@
  *   fc_pool_compress_batch  <- compressed_spec + KVCachePool.transition_compressed
  *                              kv.py:173-194, pool.py:167-192; driven per batch from
  *                              Simulator._on_stage_complete(COMPRESS) engine.py:501-510
+ *   fc_pool_compress_host_batch <- same as fc_pool_compress_batch, raw KV still in pinned
+ *                              host memory (the P.Store -> compress hand-off)
  *   fc_pool_append          <- KVCachePool.append_decode_tokens pool.py:194-211
  *   fc_pool_release_batch   <- KVCachePool.release             pool.py:213-224  (batched)
  *   fc_pool_get_stats       <- KVCachePool.stats / verify_conservation pool.py:228-257
@@ -172,6 +174,22 @@ FC_API fc_status fc_pool_compress_batch(fc_pool* pool, int32_t n, const int64_t*
                                  const int64_t* seg_tokens, const fc_press_config* press,
                                  const fc_press_inputs* inputs, const fc_press_outputs* outputs,
                                  uint64_t* requested_out, uint64_t* available_out, void* stream);
+
+/* fc_pool_compress_batch for raw KV that is still in pinned host memory:
+ * host_kv[i] is request i's dense [L][2][Hkv][T_i][D] buffer in the pool
+ * dtype (cudaHostAlloc / torch pin_memory; it must stay valid until the
+ * stream reaches this call's work). Pooled Knorm / SnapKV move only the K
+ * planes (DMA, double-buffered through pool-owned staging) and, after
+ * selection, the kept V rows (zero-copy gather): 0.5 R + 0.5 C bytes over
+ * PCIe instead of R. Other presses and legacy mode copy all of K and V. The
+ * handles' raw blocks receive the payload; the result equals
+ * fc_pool_store_tokens of every request followed by fc_pool_compress_batch. */
+FC_API fc_status fc_pool_compress_host_batch(fc_pool* pool, int32_t n, const int64_t* handle_ids,
+                                      const int64_t* seg_tokens, const fc_press_config* press,
+                                      const fc_press_inputs* inputs,
+                                      const fc_press_outputs* outputs, const void* const* host_kv,
+                                      uint64_t* requested_out, uint64_t* available_out,
+                                      void* stream);
 
 /* Grow n COMPRESSED handles by tokens[i] decode tokens (pool.py:194-211). */
 FC_API fc_status fc_pool_append(fc_pool* pool, int32_t n, const int64_t* handle_ids,

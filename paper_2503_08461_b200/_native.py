@@ -42,7 +42,7 @@ EXPORTS = (
     "fc_pool_arena", "fc_pool_alloc_batch", "fc_pool_compress_batch", "fc_pool_append",
     "fc_pool_release_batch", "fc_pool_get_stats", "fc_pool_synchronize", "fc_pool_block_table",
     "fc_pool_store_tokens", "fc_pool_load_tokens", "fc_synth_fill", "fc_compress_tensor",
-    "fc_pool_set_profiling", "fc_pool_last_profile",
+    "fc_pool_set_profiling", "fc_pool_last_profile", "fc_pool_compress_host_batch",
 )
 
 
@@ -115,6 +115,10 @@ _SIGS = {
     "fc_pool_compress_batch": (_I32, [_P, _I32, _PI64, _PI64, ctypes.POINTER(PressConfigC),
                                       ctypes.POINTER(PressInputsC), ctypes.POINTER(PressOutputsC),
                                       _PU64, _PU64, _P]),
+    "fc_pool_compress_host_batch": (_I32, [_P, _I32, _PI64, _PI64, ctypes.POINTER(PressConfigC),
+                                           ctypes.POINTER(PressInputsC),
+                                           ctypes.POINTER(PressOutputsC), ctypes.POINTER(_P),
+                                           _PU64, _PU64, _P]),
     "fc_pool_append": (_I32, [_P, _I32, _PI64, _PI64, _PU64, _PU64, _P]),
     "fc_pool_release_batch": (_I32, [_P, _I32, _PI64, _P]),
     "fc_pool_get_stats": (_I32, [_P, ctypes.POINTER(PoolStatsC)]),

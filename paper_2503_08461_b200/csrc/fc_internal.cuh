@@ -64,6 +64,17 @@ struct PressBatch {
   PressReq req[kMaxBatch];
 };
 
+// One request of a host-resident gather (fc_pool_compress_host_batch).
+struct HostGatherReq {
+  int32_t slot, T, K, reserved;
+  int64_t kept_off;   // element offset of the request's [L][H][K] kept indices
+  const char* host;   // device-mapped pointer of the pinned host [L][2][H][T][D] buffer
+};
+struct HostGatherBatch {
+  int32_t n, reserved;
+  HostGatherReq req[kMaxBatch];
+};
+
 struct PressParams {
   int32_t kind, factor, window, pool_kernel, n_sink, num_q_heads;
   // SEEDEDLINEAR: device table [factor][factor]; row m-1 = the reference's
@@ -167,7 +178,11 @@ fc_status launch_synth(const Geom& g, int dtype, char* arena, const int32_t* tab
                        const int32_t* slots, const int32_t* tokens, const uint64_t* keys,
                        uint64_t seed, int dist, cudaStream_t stream);
 fc_status launch_store(const Geom& g, char* arena, const int32_t* table_row, int64_t tok_begin,
-                       int64_t n_tok, const void* src, bool to_blocks, cudaStream_t stream);
+                       int64_t n_tok, const void* src, bool to_blocks, cudaStream_t stream,
+                       int kv0 = 0, int nkv = 2);
+fc_status launch_gather_host(const Geom& g, char* arena, const int32_t* table, int n,
+                             const HostGatherReq* reqs, const int32_t* kept_idx, int kv,
+                             cudaStream_t stream);
 fc_status launch_compress_tensor(const void* src, int64_t n, int64_t d, int dtype,
                                  const PressParams& pp, void* dst, cudaStream_t stream);
 

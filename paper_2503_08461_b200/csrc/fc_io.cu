@@ -105,13 +105,15 @@ fc_status launch_synth(const Geom& g, int dtype, char* arena, const int32_t* tab
 }
 
 // ---------------------------------------------------------------------------
-// dense [L][2][H][n][D] <-> paged blocks
+// dense [L][nkv][H][n][D] <-> paged blocks (nkv = 2: K and V; nkv = 1: only
+// kv plane kv0, the K-only ingest of the host-resident compress path)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
     store_tokens_kernel(char* __restrict__ arena, const int32_t* __restrict__ row_tab, const Geom g,
-                        int64_t tok_begin, int64_t n_tok, char* __restrict__ dense, int to_blocks) {
+                        int64_t tok_begin, int64_t n_tok, char* __restrict__ dense, int to_blocks,
+                        int kv0, int nkv) {
   const int vpr = (int)(g.row_bytes / 16);
-  const int64_t total = (int64_t)g.L * 2 * g.H * n_tok * vpr;
+  const int64_t total = (int64_t)g.L * nkv * g.H * n_tok * vpr;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int vec = (int)(v % vpr);
@@ -120,8 +122,8 @@ __global__ void __launch_bounds__(256)
     rest /= n_tok;
     const int h = (int)(rest % g.H);
     rest /= g.H;
-    const int kv = (int)(rest % 2);
-    const int l = (int)(rest / 2);
+    const int kv = kv0 + (int)(rest % nkv);
+    const int l = (int)(rest / nkv);
     const int64_t t = tok_begin + i;
     char* blk = arena + g.seg_base(l, kv, h) + (int64_t)row_tab[t / g.bs] * g.block_stride +
                 (t % g.bs) * g.row_bytes + vec * 16;
@@ -134,15 +136,88 @@ __global__ void __launch_bounds__(256)
 }
 
 fc_status launch_store(const Geom& g, char* arena, const int32_t* table_row, int64_t tok_begin,
-                       int64_t n_tok, const void* src, bool to_blocks, cudaStream_t stream) {
+                       int64_t n_tok, const void* src, bool to_blocks, cudaStream_t stream,
+                       int kv0, int nkv) {
   if (((uintptr_t)src) % 16) return set_error(FC_ERR_INVALID_ARG, "dense buffer must be 16-byte aligned");
-  const int64_t total = (int64_t)g.L * 2 * g.H * n_tok * (g.row_bytes / 16);
+  const int64_t total = (int64_t)g.L * nkv * g.H * n_tok * (g.row_bytes / 16);
   int64_t grid = (total + 255) / 256;
   if (grid > 148 * 16) grid = 148 * 16;
   store_tokens_kernel<<<(unsigned)grid, 256, 0, stream>>>(arena, table_row, g, tok_begin, n_tok,
-                                                          (char*)src, to_blocks ? 1 : 0);
+                                                          (char*)src, to_blocks ? 1 : 0, kv0, nkv);
   note_launch();
   return cuda_check(cudaGetLastError(), "store_tokens_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Host-resident compress, second half: kept V rows read straight from pinned
+// host memory (zero-copy over PCIe, UVA) into rank slots of the request's
+// blocks. Host layout per request: [L][2][H][T][D]; V row (l, h, t) is
+// row_bytes contiguous bytes. Every thread keeps kUnroll 16-B loads in flight
+// so the PCIe read pipe (~2 us latency) stays full; measured 51.5 GB/s for
+// 256-B rows at 25-50% density (scripts/pcie_probe.cu).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    gather_host_rows_kernel(char* __restrict__ arena, const int32_t* __restrict__ table,
+                            const Geom g, const __grid_constant__ HostGatherBatch b,
+                            const int32_t* __restrict__ kept_idx, int kv) {
+  constexpr int kUnroll = 4;
+  const HostGatherReq q = b.req[blockIdx.y];
+  const int vpr = (int)(g.row_bytes / 16);
+  const int64_t total = (int64_t)g.L * g.H * q.K * vpr;
+  const int32_t* row_tab = table + (int64_t)q.slot * g.max_bpr;
+  const int32_t* idx = kept_idx + q.kept_off;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < total;
+       v0 += stride * kUnroll) {
+    uint4 buf[kUnroll];
+    char* dst[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t v = v0 + u * stride;
+      dst[u] = nullptr;
+      if (v < total) {
+        const int vec = (int)(v % vpr);
+        const int64_t rest = v / vpr;           // (l*H + h)*K + j
+        const int j = (int)(rest % q.K);
+        const int lh = (int)(rest / q.K);
+        const int l = lh / g.H, h = lh % g.H;
+        const int src = idx[rest];
+        buf[u] = ld_stream(q.host + ((((int64_t)l * 2 + kv) * g.H + h) * q.T + src) * g.row_bytes +
+                           vec * 16);
+        dst[u] = arena + g.seg_base(l, kv, h) + (int64_t)row_tab[j >> g.bs_shift] * g.block_stride +
+                 (int64_t)(j & (g.bs - 1)) * g.row_bytes + vec * 16;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (dst[u]) st_stream(dst[u], buf[u]);
+  }
+}
+
+fc_status launch_gather_host(const Geom& g, char* arena, const int32_t* table, int n,
+                             const HostGatherReq* reqs, const int32_t* kept_idx, int kv,
+                             cudaStream_t stream) {
+  for (int c = 0; c < n; c += kMaxBatch) {
+    HostGatherBatch b;
+    memset(&b, 0, sizeof(b));
+    b.n = n - c < kMaxBatch ? n - c : kMaxBatch;
+    int64_t max_vecs = 0;
+    for (int i = 0; i < b.n; ++i) {
+      b.req[i] = reqs[c + i];
+      const int64_t vv = (int64_t)g.L * g.H * b.req[i].K * (g.row_bytes / 16);
+      max_vecs = vv > max_vecs ? vv : max_vecs;
+    }
+    int64_t gx = (max_vecs + 1023) / 1024;
+    const int64_t cap = (148LL * 8 + b.n - 1) / b.n;
+    if (gx > cap) gx = cap;
+    if (gx < 1) gx = 1;
+    gather_host_rows_kernel<<<dim3((unsigned)gx, (unsigned)b.n), 256, 0, stream>>>(arena, table, g, b,
+                                                                                  kept_idx, kv);
+    note_launch();
+    fc_status st = cuda_check(cudaGetLastError(), "gather_host_rows_kernel");
+    if (st != FC_OK) return st;
+  }
+  return FC_OK;
 }
 
 // ---------------------------------------------------------------------------

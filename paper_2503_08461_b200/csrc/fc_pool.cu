@@ -136,6 +136,15 @@ struct fc_pool {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, press_end, free_end, end
   int64_t prof_press_launches = 0, prof_total_launches = 0;
   bool prof_valid = false;
+  // host-resident compress (fc_pool_compress_host_batch): a copy stream, two
+  // staging slots the DMA fills while the previous slot is scattered into
+  // blocks, and a kept-index scratch for the zero-copy V gather.
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t hev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // start, copied[2], scattered[2]
+  char* d_stage[2] = {nullptr, nullptr};
+  uint64_t stage_bytes = 0;
+  int32_t* d_kept = nullptr;
+  int64_t kept_cap = 0;
 };
 
 namespace {
@@ -339,8 +348,14 @@ fc_status fc_pool_destroy(fc_pool* p) {
   cudaFree(p->d_err);
   cudaFree(p->d_wtable);
   cudaFree(p->d_ws);
+  cudaFree(p->d_stage[0]);
+  cudaFree(p->d_stage[1]);
+  cudaFree(p->d_kept);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : p->hev)
+    if (e) cudaEventDestroy(e);
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   delete p;
   return FC_OK;
 }
@@ -405,20 +420,25 @@ fc_status fc_pool_alloc_batch(fc_pool* p, int32_t n, const int64_t* request_ids,
   return run_block_ops(p, ops, true, false, {}, (cudaStream_t)stream);
 }
 
-fc_status fc_pool_compress_batch(fc_pool* p, int32_t n, const int64_t* handle_ids,
-                                 const int64_t* seg_tokens, const fc_press_config* press,
-                                 const fc_press_inputs* inputs, const fc_press_outputs* outputs,
-                                 uint64_t* requested_out, uint64_t* available_out, void* stream_) {
+namespace {
+
+// Every check of a compress call, before any mutation (the batch is atomic).
+// Fills the slot and K_r (total, first segment) of every member.
+fc_status check_compress(fc_pool* p, int32_t n, const int64_t* handle_ids, const int64_t* seg_tokens,
+                         const fc_press_config* press, const fc_press_inputs* inputs,
+                         std::vector<int32_t>& slot, std::vector<int32_t>& kept,
+                         std::vector<int32_t>& kept0, uint64_t* requested_out,
+                         uint64_t* available_out) {
   if (!p || !press || n < 0 || (n > 0 && (!handle_ids || !seg_tokens)))
     return set_error(FC_ERR_INVALID_ARG, "bad arguments");
   if (press->factor < 1) return set_error(FC_ERR_INVALID_ARG, "factor must be >= 1");
   if (press->kind < FC_PRESS_KNORM || press->kind > FC_PRESS_SEEDEDLINEAR)
     return set_error(FC_ERR_INVALID_ARG, "unknown press kind %d", press->kind);
-  cudaStream_t stream = (cudaStream_t)stream_;
   const bool legacy = p->mode == FC_LEGACY_ZOMBIE;
   const int bs = p->g.bs;
-  std::vector<int32_t> slot(n);
-  std::vector<int32_t> kept(n), kept0(n);
+  slot.assign(n, 0);
+  kept.assign(n, 0);
+  kept0.assign(n, 0);
   uint64_t cur = p->current;
   int64_t new_blocks = 0;
   for (int i = 0; i < n; ++i) {
@@ -466,10 +486,24 @@ fc_status fc_pool_compress_batch(fc_pool* p, int32_t n, const int64_t* handle_id
     return set_error(FC_ERR_INVALID_ARG, "num_q_heads must be a multiple of num_kv_heads");
   if (press->kind == FC_PRESS_SEEDEDLINEAR && (press->factor > 64 || !press->chunk_weights))
     return set_error(FC_ERR_UNSUPPORTED, "seeded-linear in-pool compression needs factor <= 64 and weights");
-  if (n == 0) return FC_OK;
+  return FC_OK;
+}
+
+}  // namespace
+
+fc_status fc_pool_compress_batch(fc_pool* p, int32_t n, const int64_t* handle_ids,
+                                 const int64_t* seg_tokens, const fc_press_config* press,
+                                 const fc_press_inputs* inputs, const fc_press_outputs* outputs,
+                                 uint64_t* requested_out, uint64_t* available_out, void* stream_) {
+  std::vector<int32_t> slot, kept, kept0;
+  fc_status st = check_compress(p, n, handle_ids, seg_tokens, press, inputs, slot, kept, kept0,
+                                requested_out, available_out);
+  if (st != FC_OK || n == 0) return st;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const bool legacy = p->mode == FC_LEGACY_ZOMBIE;
+  const int bs = p->g.bs;
 
   DeviceGuard guard(p->device);
-  fc_status st;
   const int64_t launches0 = g_launches;
   if (p->profiling) cudaEventRecord(p->ev[0], stream);
   // Legacy: move the raw rows aside and pop fresh destination blocks (batch order).
@@ -598,6 +632,122 @@ fc_status fc_pool_compress_batch(fc_pool* p, int32_t n, const int64_t* handle_id
     sl.state = ST_COMPRESSED;
   }
   return FC_OK;
+}
+
+// Host-resident compress: request i's raw KV is a pinned host buffer
+// [L][2][H][T_i][D]. Split path (pooled Knorm / SnapKV, whose scores read only
+// K): DMA the K planes through two staging slots on the pool's copy stream
+// (slot i+1 fills while slot i is scattered into blocks), compress, then read
+// only the kept V rows over PCIe (gather_host_rows_kernel) -- 0.5 R + 0.5 C
+// bytes cross PCIe instead of R. Other presses / legacy mode DMA all of K and V.
+fc_status fc_pool_compress_host_batch(fc_pool* p, int32_t n, const int64_t* handle_ids,
+                                      const int64_t* seg_tokens, const fc_press_config* press,
+                                      const fc_press_inputs* inputs,
+                                      const fc_press_outputs* outputs, const void* const* host_kv,
+                                      uint64_t* requested_out, uint64_t* available_out,
+                                      void* stream_) {
+  std::vector<int32_t> slot, kept, kept0;
+  fc_status st = check_compress(p, n, handle_ids, seg_tokens, press, inputs, slot, kept, kept0,
+                                requested_out, available_out);
+  if (st != FC_OK || n == 0) return st;
+  if (!host_kv) return set_error(FC_ERR_INVALID_ARG, "host_kv missing");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  DeviceGuard guard(p->device);
+  const Geom& g = p->g;
+  const bool split = p->mode == FC_POOLED &&
+                     (press->kind == FC_PRESS_KNORM || press->kind == FC_PRESS_SNAPKV);
+  std::vector<const char*> dev_host(n);
+  uint64_t max_stage = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!host_kv[i] || ((uintptr_t)host_kv[i]) % 16)
+      return set_error(FC_ERR_INVALID_ARG, "host_kv[%d] missing or not 16-byte aligned", i);
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, host_kv[i]) != cudaSuccess || at.type != cudaMemoryTypeHost ||
+        !at.devicePointer) {
+      cudaGetLastError();
+      return set_error(FC_ERR_INVALID_ARG,
+                       "host_kv[%d] must be pinned host memory (cudaHostAlloc / pin_memory)", i);
+    }
+    dev_host[i] = (const char*)at.devicePointer;
+    const uint64_t plane = (uint64_t)g.H * p->slots[slot[i]].tokens * g.row_bytes;
+    max_stage = std::max<uint64_t>(max_stage, plane * g.L * (split ? 1 : 2));
+  }
+  if (!p->copy_stream) {
+    st = cuda_check(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking),
+                    "cudaStreamCreate(copy)");
+    for (auto& e : p->hev)
+      if (st == FC_OK) st = cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    if (st != FC_OK) return st;
+  }
+  if (max_stage > p->stage_bytes) {
+    cudaStreamSynchronize(p->copy_stream);
+    cudaStreamSynchronize(stream);
+    for (auto& b : p->d_stage) {
+      cudaFree(b);
+      b = nullptr;
+    }
+    p->stage_bytes = 0;
+    for (auto& b : p->d_stage) {
+      st = cuda_check(cudaMalloc(&b, max_stage), "cudaMalloc(staging)");
+      if (st != FC_OK) return st;
+    }
+    p->stage_bytes = max_stage;
+  }
+  // Ingest: DMA into staging slot i%2 on the copy stream, scatter on `stream`.
+  cudaEventRecord(p->hev[0], stream);
+  cudaStreamWaitEvent(p->copy_stream, p->hev[0], 0);
+  for (int i = 0; i < n; ++i) {
+    const int b = i & 1;
+    const int64_t T = p->slots[slot[i]].tokens;
+    const size_t plane = (size_t)g.H * T * g.row_bytes;
+    if (i >= 2) cudaStreamWaitEvent(p->copy_stream, p->hev[3 + b], 0);
+    if (split)
+      st = cuda_check(cudaMemcpy2DAsync(p->d_stage[b], plane, host_kv[i], 2 * plane, plane, g.L,
+                                        cudaMemcpyHostToDevice, p->copy_stream),
+                      "cudaMemcpy2DAsync(K planes)");
+    else
+      st = cuda_check(cudaMemcpyAsync(p->d_stage[b], host_kv[i], 2 * plane * g.L,
+                                      cudaMemcpyHostToDevice, p->copy_stream),
+                      "cudaMemcpyAsync(KV)");
+    if (st != FC_OK) return st;
+    cudaEventRecord(p->hev[1 + b], p->copy_stream);
+    cudaStreamWaitEvent(stream, p->hev[1 + b], 0);
+    st = launch_store(g, p->arena, p->d_table + (int64_t)slot[i] * g.max_bpr, 0, T, p->d_stage[b],
+                      true, stream, 0, split ? 1 : 2);
+    if (st != FC_OK) return st;
+    cudaEventRecord(p->hev[3 + b], stream);
+  }
+  // Compress on the device-resident K (and V); the split path needs the kept indices.
+  fc_press_outputs outs{};
+  if (outputs) outs = *outputs;
+  const int64_t LH = (int64_t)g.L * g.H;
+  int64_t sum_kept = 0;
+  for (int i = 0; i < n; ++i) sum_kept += (int64_t)kept[i] * LH;
+  if (split && !outs.kept_idx) {
+    if (sum_kept > p->kept_cap) {
+      cudaStreamSynchronize(stream);
+      cudaFree(p->d_kept);
+      p->d_kept = nullptr;
+      p->kept_cap = 0;
+      st = cuda_check(cudaMalloc(&p->d_kept, sum_kept * sizeof(int32_t)), "cudaMalloc(kept)");
+      if (st != FC_OK) return st;
+      p->kept_cap = sum_kept;
+    }
+    outs.kept_idx = p->d_kept;
+  }
+  st = fc_pool_compress_batch(p, n, handle_ids, seg_tokens, press, inputs, &outs, requested_out,
+                              available_out, stream_);
+  if (st != FC_OK || !split) return st;
+  // Kept V rows: zero-copy reads of the pinned host buffers into rank slots.
+  std::vector<HostGatherReq> reqs(n);
+  int64_t ko = 0;
+  for (int i = 0; i < n; ++i) {
+    reqs[i] = HostGatherReq{slot[i], 0, kept[i], 0, ko, dev_host[i]};
+    ko += (int64_t)kept[i] * LH;
+  }
+  // raw T of request i = the sum of its segments (the slot now holds K_r)
+  for (int i = 0; i < n; ++i) reqs[i].T = (int32_t)(seg_tokens[2 * i] + seg_tokens[2 * i + 1]);
+  return launch_gather_host(g, p->arena, p->d_table, n, reqs.data(), outs.kept_idx, 1, stream);
 }
 
 fc_status fc_pool_append(fc_pool* p, int32_t n, const int64_t* handle_ids, const int64_t* tokens,

@@ -259,7 +259,7 @@ class _NativePool:
         return [int(out[i]) for i in range(n)]
 
     def compress(self, handle_ids, seg_tokens, comp: CompressorSpec, num_q_heads: int,
-                 inputs, kept_out, scores_out) -> None:
+                 inputs, kept_out, scores_out, host_kv=None) -> None:
         kind = {
             PressKind.KNORM: nat.PRESS_KNORM,
             PressKind.SNAPKV: nat.PRESS_SNAPKV,
@@ -280,9 +280,16 @@ class _NativePool:
         outs = nat.PressOutputsC(kept_out, scores_out)
         segs = [int(x) for pair in seg_tokens for x in pair]
         req, avail = ctypes.c_uint64(), ctypes.c_uint64()
-        self._check(self.lib.fc_pool_compress_batch(
+        if host_kv is None:
+            self._check(self.lib.fc_pool_compress_batch(
+                self.ptr, len(handle_ids), nat.i64_array(handle_ids), nat.i64_array(segs),
+                ctypes.byref(cfg), ctypes.byref(ins), ctypes.byref(outs), ctypes.byref(req),
+                ctypes.byref(avail), self.stream()), req, avail)
+            return
+        ptrs = (ctypes.c_void_p * max(1, len(host_kv)))(*[int(p) for p in host_kv])
+        self._check(self.lib.fc_pool_compress_host_batch(
             self.ptr, len(handle_ids), nat.i64_array(handle_ids), nat.i64_array(segs),
-            ctypes.byref(cfg), ctypes.byref(ins), ctypes.byref(outs), ctypes.byref(req),
+            ctypes.byref(cfg), ctypes.byref(ins), ctypes.byref(outs), ptrs, ctypes.byref(req),
             ctypes.byref(avail), self.stream()), req, avail)
 
     def append(self, handle_ids, tokens) -> None:
@@ -488,7 +495,7 @@ class KVCachePool:
     def compress_batch(self, handles: Sequence[CacheHandle], comp: CompressorSpec | None = None,
                        now: float = 0.0, *, q_window=None, mean_q=None, cov_q=None,
                        return_indices: bool = False, return_scores: bool = False,
-                       new_specs: Sequence[KVCacheSpec] | None = None):
+                       new_specs: Sequence[KVCacheSpec] | None = None, host_kv=None):
         """Compress many RAW handles in one batched device pass, then transition them.
 
         ``comp.press`` picks the scorer; every member keeps exactly
@@ -500,6 +507,13 @@ class KVCachePool:
         transitions follow in batch order with the same ``now``
         (engine.py:501-510). Returns ``CompressResult`` when indices/scores
         are requested, else the handles.
+
+        ``host_kv`` (optional): one pinned CPU tensor [L, 2, H, T_r, D] per
+        handle holding its raw KV (the prefill output not yet in the pool).
+        The library moves it into the handle's blocks as part of the call;
+        for pooled Knorm / SnapKV only the K planes and the kept V rows cross
+        PCIe (``fc_pool_compress_host_batch``). The tensors must stay alive
+        until the pool's stream has run this call.
         """
         comp = comp or self.compressor
         handles = list(handles)
@@ -523,7 +537,9 @@ class KVCachePool:
         result = None
         if self._native is not None and handles:
             result = self._device_compress(handles, new_specs, comp, q_window, mean_q, cov_q,
-                                           return_indices, return_scores)
+                                           return_indices, return_scores, host_kv)
+        elif host_kv is not None:
+            raise nat.NativeUnavailable("host_kv needs a device pool (pass device=...)")
         for h, spec in zip(handles, new_specs):
             self._transition_ledger(h, spec, now)
         if return_indices or return_scores:
@@ -531,9 +547,22 @@ class KVCachePool:
         return handles
 
     def _device_compress(self, handles, new_specs, comp, q_window, mean_q, cov_q,
-                         return_indices, return_scores):
+                         return_indices, return_scores, host_kv=None):
         torch = self._native.torch
         cfg = self.config
+        host_ptrs = None
+        if host_kv is not None:
+            host_kv = list(host_kv)
+            if len(host_kv) != len(handles):
+                raise ValueError("host_kv needs one tensor per handle")
+            host_ptrs = []
+            for h, t in zip(handles, host_kv):
+                want = (cfg.num_layers, 2, cfg.num_kv_heads, h.spec.total_tokens, cfg.head_dim)
+                if tuple(t.shape) != want or t.dtype != self._native.torch_dtype \
+                        or t.device.type != "cpu" or not t.is_pinned() or not t.is_contiguous():
+                    raise ValueError(f"host_kv tensors must be contiguous pinned CPU "
+                                     f"{self._native.kv_dtype} tensors of shape {want}")
+                host_ptrs.append(t.data_ptr())
         lh = cfg.num_layers * cfg.num_kv_heads
         n = len(handles)
         segs = []
@@ -575,7 +604,8 @@ class KVCachePool:
             scores_t = torch.empty(sum(raw) * lh, dtype=torch.float32, device=dev)
         self._native.compress([h.handle_id for h in handles], segs, comp, hq, inputs,
                               kept_t.data_ptr() if kept_t is not None else None,
-                              scores_t.data_ptr() if scores_t is not None else None)
+                              scores_t.data_ptr() if scores_t is not None else None,
+                              host_ptrs)
         if not (return_indices or return_scores):
             return None
         res = CompressResult(kept_idx=[], scores=[])
