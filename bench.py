@@ -47,6 +47,9 @@ CONFIGS = {
            "wave of config 4)",
     "c4": "ExpectedAttention at 25% keep on 256 mixed-length requests (1k-8k tokens) with pool "
           "alloc/free churn (admission waves, 140 GB pool) and fragmentation accounting",
+    "c2d": "decode after compression: config 2's batch (32 x 1088 tokens, Knorm 50% -> 544) "
+           "then 64 decode steps, each = append one token per request + per layer write K/V and "
+           "paged attention over the compacted blocks (SURVEY.md §8(f) row 2)",
     "c5": "synthetic serving trace at 40 req/s (2000 requests, highload shape), request-sharded "
           "by NCCL occupancy exchange, mixed Knorm/SnapKV, TTFT and compression throughput",
 }
@@ -324,6 +327,96 @@ def run_churn_bench(args, rank, world, local_rank):
     }
 
 
+def run_decode_bench(args, rank, world, local_rank):
+    """Decode over compacted blocks: tokens/s of decode steps and the attention kernel's HBM
+    roofline (K/V bytes of every live token, every layer)."""
+    import torch
+
+    from paper_2503_08461_b200 import KVCachePool, kv_bytes
+
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    cfg, dtype, specs, comp = workload("c2")
+    n, L, H, D = len(specs), cfg.num_layers, cfg.num_kv_heads, cfg.head_dim
+    steps_per_run = 64
+    cap = sum(kv_bytes(cfg, s.total_tokens) for s in specs)
+    pool = KVCachePool(cfg, cap, device=device, kv_dtype=dtype, max_handles=2 * n,
+                       max_tokens_per_handle=max(s.total_tokens for s in specs) + 64,
+                       num_q_heads=H)
+    tdt = getattr(torch, dtype)
+    gen = torch.Generator(device=device).manual_seed(rank)
+    k = torch.randn((L, n, H, D), generator=gen, device=device).to(tdt)
+    v = torch.randn((L, n, H, D), generator=gen, device=device).to(tdt)
+    q = torch.randn((L, n, H, D), generator=gen, device=device).to(tdt)
+    out = torch.empty((n, H, D), dtype=tdt, device=device)
+    stream = torch.cuda.current_stream(device)
+    rids = [rank * 1_000_000 + i for i in range(n)]
+    step_ms, attn_ms, attn_bytes, launches = [], [], 0, 0
+    from paper_2503_08461_b200 import _native
+
+    def run(timed):
+        nonlocal attn_bytes, launches
+        hs = pool.allocate_batch(rids, specs, 0.0)
+        pool.synth_fill(hs, seed=17)
+        pool.compress_batch(hs, comp, 1.0)
+        torch.cuda.synchronize(device)
+        for st in range(steps_per_run):
+            l0 = _native.launch_count()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * L + 2)]
+            ev[0].record(stream)
+            pool.append_decode_batch(hs, 1, 2.0 + st)
+            for layer in range(L):
+                pool.write_decode_kv(hs, layer, k[layer], v[layer])
+                ev[1 + 2 * layer].record(stream)
+                pool.decode_attention(hs, layer, q[layer], out=out)
+                ev[2 + 2 * layer].record(stream)
+            ev[-1].record(stream)
+            ev[-1].synchronize()
+            if timed:
+                step_ms.append(ev[0].elapsed_time(ev[-1]))
+                attn_ms.append(sum(ev[1 + 2 * i].elapsed_time(ev[2 + 2 * i]) for i in range(L)) / L)
+                live = sum(h.spec.total_tokens for h in hs)
+                attn_bytes += live * 2 * H * D * cfg.bytes_per_element + 2 * n * H * D * cfg.bytes_per_element
+                launches += _native.launch_count() - l0
+        pool.release_batch(hs, 99.0)
+
+    for _ in range(args.warmup):
+        run(False)
+    torch.cuda.synchronize(device)
+    if world > 1:
+        torch.distributed.barrier()
+    with ClockSampler(device.index) as clocks:
+        for _ in range(args.steps):
+            run(True)
+        torch.cuda.synchronize(device)
+    if world > 1:
+        torch.distributed.barrier()
+    total_ms = sum(step_ms)
+    max_ms = _allreduce(total_ms, "max", device)
+    n_steps = len(step_ms)
+    peak, peak_kind = measured_peak()
+    per_launch_bytes = attn_bytes / (n_steps)               # per layer-launch average
+    achieved = per_launch_bytes / (statistics.mean(attn_ms) / 1e3) / 1e9
+    return {
+        "metric": "decode tokens/s over compressed caches", "value": n * n_steps * world / (max_ms / 1e3),
+        "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": max_ms / n_steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16", "data": "synthetic (K8 generator; random q/k/v)",
+        "config": {"workload": f"c2d: {CONFIGS['c2d']}", "requests_per_gpu": n,
+                   "decode_steps_per_run": steps_per_run, "layers": L,
+                   "timing": "CUDA events per decode step (append + 32 x (write K/V + attention)); "
+                             "attention kernel events per layer"},
+        "roofline": {"bound": "hbm", "kernel": "decode_attn_kernel (paged, split-KV)",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "alg_bytes_per_launch": per_launch_bytes,
+                     "attn_us_per_layer": 1e3 * statistics.mean(attn_ms)},
+        "tpot_ms": max_ms / n_steps,
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -530,7 +623,7 @@ def _cpu_model():
 
 
 def run_reference(args):
-    cfg, dtype, specs, comp = workload(args.config if args.config != "c5" else "c2")
+    cfg, dtype, specs, comp = workload(args.config if args.config not in ("c5", "c2d") else "c2")
     times = []
     last = None
     for i in range(args.warmup + args.steps):
@@ -590,10 +683,12 @@ def main():
         result = run_churn_bench(args, rank, world, local_rank)
     elif args.config == "c5":
         result = run_serving_bench(args, rank, world, local_rank)
+    elif args.config == "c2d":
+        result = run_decode_bench(args, rank, world, local_rank)
     else:
         result = run_ours(args, rank, world, local_rank)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cfg, dtype, specs, comp = workload(args.config if args.config != "c5" else "c2")
+        cfg, dtype, specs, comp = workload(args.config if args.config not in ("c5", "c2d") else "c2")
         result["cpu_baseline"] = cpu_reference(args, cfg, dtype, specs, comp)
     if rank == 0:
         print(json.dumps(result), flush=True)

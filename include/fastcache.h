@@ -19,6 +19,9 @@
  *   fc_pool_compress_host_batch <- same as fc_pool_compress_batch, raw KV still in pinned
  *                              host memory (the P.Store -> compress hand-off)
  *   fc_pool_append          <- KVCachePool.append_decode_tokens pool.py:194-211
+ *   fc_pool_write_kv / fc_pool_decode_attention <- the decode stage over compressed
+ *                              caches (engine.py:514-548 drives append_decode_tokens per
+ *                              step; UpdateKVCache PAPER.md:255-261)
  *   fc_pool_release_batch   <- KVCachePool.release             pool.py:213-224  (batched)
  *   fc_pool_get_stats       <- KVCachePool.stats / verify_conservation pool.py:228-257
  *   fc_compress_tensor      <- compress_tensor                 kv.py:211-239
@@ -195,6 +198,19 @@ FC_API fc_status fc_pool_compress_host_batch(fc_pool* pool, int32_t n, const int
 FC_API fc_status fc_pool_append(fc_pool* pool, int32_t n, const int64_t* handle_ids,
                          const int64_t* tokens, uint64_t* requested_out, uint64_t* available_out,
                          void* stream);
+
+/* Decode over the compacted blocks, one layer at a time. fc_pool_write_kv
+ * writes one token's K and V per handle (k, v: [n][Hkv][D], pool dtype) at
+ * positions[i] (NULL: the handle's last token, i.e. the slot fc_pool_append
+ * just added). fc_pool_decode_attention computes, for each handle i and query
+ * head j, softmax(scale * q_ij . K^T) V over the handle's live tokens in
+ * layer `layer` (q, out: [n][num_q_heads][D], pool dtype; scale <= 0 means
+ * 1/sqrt(D); fp32 accumulation). */
+FC_API fc_status fc_pool_write_kv(fc_pool* pool, int32_t layer, int32_t n, const int64_t* handle_ids,
+                           const int64_t* positions, const void* k, const void* v, void* stream);
+FC_API fc_status fc_pool_decode_attention(fc_pool* pool, int32_t layer, int32_t n,
+                                   const int64_t* handle_ids, int32_t num_q_heads, float scale,
+                                   const void* q, void* out, void* stream);
 
 /* Release n handles, pushing their blocks (request order, ascending logical
  * block) onto the device free stack (pool.py:213-224). */

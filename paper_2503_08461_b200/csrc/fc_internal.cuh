@@ -75,6 +75,26 @@ struct HostGatherBatch {
   HostGatherReq req[kMaxBatch];
 };
 
+// Decode over the compacted blocks (fc_decode.cu).
+constexpr int kMaxDecode = 256;     // requests per decode launch
+struct DecodeReq {
+  int32_t slot, T;     // block-table row, live tokens
+  int32_t item0;       // first CTA of this request (items = H * nsplit)
+  int32_t nsplit;      // KV splits per kv head
+  int32_t q_row;       // row of q / out
+};
+struct DecodeBatch {
+  int32_t n, Hq, layer, split_tokens, items;
+  DecodeReq req[kMaxDecode];
+};
+struct KVWriteReq {
+  int32_t slot, pos, row;
+};
+struct KVWriteBatch {
+  int32_t n, layer;
+  KVWriteReq req[kMaxDecode];
+};
+
 struct PressParams {
   int32_t kind, factor, window, pool_kernel, n_sink, num_q_heads;
   // SEEDEDLINEAR: device table [factor][factor]; row m-1 = the reference's
@@ -172,6 +192,14 @@ fc_status launch_ea_tc(const Geom& g, char* arena, const int32_t* table, const P
                        const PressParams& pp, const fc_press_inputs& in, const fc_press_outputs& out,
                        int max_K, cudaStream_t stream);
 int64_t press_workspace_floats(const Geom& g, int kind, int window, int num_q_heads, int max_T);
+
+// decode kernels (fc_decode.cu)
+fc_status launch_decode_attention(const Geom& g, int dtype, const char* arena, const int32_t* table,
+                                  const DecodeBatch& b, int gq, const void* q, void* out,
+                                  float scale_log2, float* ws, int32_t* counters,
+                                  cudaStream_t stream);
+fc_status launch_write_kv(const Geom& g, char* arena, const int32_t* table, const KVWriteBatch& b,
+                          const void* k, const void* v, cudaStream_t stream);
 
 // io kernels (fc_io.cu)
 fc_status launch_synth(const Geom& g, int dtype, char* arena, const int32_t* table, int n,

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <unordered_map>
 #include <vector>
@@ -145,6 +146,10 @@ struct fc_pool {
   uint64_t stage_bytes = 0;
   int32_t* d_kept = nullptr;
   int64_t kept_cap = 0;
+  // decode attention: split-KV partials and per-(request, kv head) arrival counters
+  float* d_dec_ws = nullptr;
+  int64_t dec_ws_floats = 0;
+  int32_t* d_dec_ctr = nullptr;
 };
 
 namespace {
@@ -351,6 +356,8 @@ fc_status fc_pool_destroy(fc_pool* p) {
   cudaFree(p->d_stage[0]);
   cudaFree(p->d_stage[1]);
   cudaFree(p->d_kept);
+  cudaFree(p->d_dec_ws);
+  cudaFree(p->d_dec_ctr);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : p->hev)
@@ -727,6 +734,8 @@ fc_status fc_pool_compress_host_batch(fc_pool* p, int32_t n, const int64_t* hand
     if (sum_kept > p->kept_cap) {
       cudaStreamSynchronize(stream);
       cudaFree(p->d_kept);
+  cudaFree(p->d_dec_ws);
+  cudaFree(p->d_dec_ctr);
       p->d_kept = nullptr;
       p->kept_cap = 0;
       st = cuda_check(cudaMalloc(&p->d_kept, sum_kept * sizeof(int32_t)), "cudaMalloc(kept)");
@@ -851,6 +860,113 @@ fc_status fc_pool_release_batch(fc_pool* p, int32_t n, const int64_t* handle_ids
     p->h2s.erase(sl.handle_id);
     sl = Slot();
     p->free_slots.push_back(slot[i]);
+  }
+  return FC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// decode over the compacted blocks
+// ---------------------------------------------------------------------------
+fc_status fc_pool_write_kv(fc_pool* p, int32_t layer, int32_t n, const int64_t* handle_ids,
+                           const int64_t* positions, const void* k, const void* v, void* stream) {
+  if (!p || n < 0 || (n > 0 && (!handle_ids || !k || !v)))
+    return set_error(FC_ERR_INVALID_ARG, "bad arguments");
+  if (layer < 0 || layer >= p->g.L) return set_error(FC_ERR_INVALID_ARG, "layer out of range");
+  if (((uintptr_t)k) % 16 || ((uintptr_t)v) % 16)
+    return set_error(FC_ERR_INVALID_ARG, "k / v must be 16-byte aligned");
+  std::vector<KVWriteReq> reqs(n);
+  for (int i = 0; i < n; ++i) {
+    int32_t s;
+    fc_status st = lookup(p, handle_ids[i], &s);
+    if (st != FC_OK) return st;
+    const int64_t T = p->slots[s].tokens;
+    const int64_t pos = positions ? positions[i] : T - 1;
+    if (pos < 0 || pos >= T) return set_error(FC_ERR_INVALID_ARG, "position %lld outside the handle's %lld tokens",
+                                              (long long)pos, (long long)T);
+    reqs[i] = KVWriteReq{s, (int32_t)pos, i};
+  }
+  DeviceGuard guard(p->device);
+  for (int c = 0; c < n; c += kMaxDecode) {
+    KVWriteBatch b;
+    memset(&b, 0, sizeof(b));
+    b.n = std::min(kMaxDecode, n - c);
+    b.layer = layer;
+    for (int i = 0; i < b.n; ++i) b.req[i] = reqs[c + i];
+    fc_status st = launch_write_kv(p->g, p->arena, p->d_table, b, k, v, (cudaStream_t)stream);
+    if (st != FC_OK) return st;
+  }
+  return FC_OK;
+}
+
+fc_status fc_pool_decode_attention(fc_pool* p, int32_t layer, int32_t n, const int64_t* handle_ids,
+                                   int32_t num_q_heads, float scale, const void* q, void* out,
+                                   void* stream) {
+  if (!p || n < 0 || (n > 0 && (!handle_ids || !q || !out)))
+    return set_error(FC_ERR_INVALID_ARG, "bad arguments");
+  if (layer < 0 || layer >= p->g.L) return set_error(FC_ERR_INVALID_ARG, "layer out of range");
+  if (num_q_heads < p->g.H || num_q_heads % p->g.H)
+    return set_error(FC_ERR_INVALID_ARG, "num_q_heads must be a multiple of num_kv_heads");
+  if (((uintptr_t)q) % 16 || ((uintptr_t)out) % 16)
+    return set_error(FC_ERR_INVALID_ARG, "q / out must be 16-byte aligned");
+  const int gq = num_q_heads / p->g.H;
+  std::vector<int32_t> slot(n);
+  int64_t total_tok = 0;
+  for (int i = 0; i < n; ++i) {
+    fc_status st = lookup(p, handle_ids[i], &slot[i]);
+    if (st != FC_OK) return st;
+    if (p->slots[slot[i]].tokens == 0) return set_error(FC_ERR_EMPTY_INPUT, "handle has no tokens");
+    total_tok += p->slots[slot[i]].tokens;
+  }
+  if (n == 0) return FC_OK;
+  if (scale <= 0.f) scale = 1.0f / sqrtf((float)p->g.D);
+  const float scale_log2 = scale * 1.4426950408889634f;
+  // Split-KV only when (request, kv head) pairs alone cannot fill one wave of
+  // 4 CTAs per SM: measured at c2d, 2-16 waves of splits cost 18-30% more
+  // than the ragged 1.7-wave unsplit grid (partials + merge + short CTAs).
+  const int64_t want_items = 148 * 4;
+  int split = 1 << 30;
+  if ((int64_t)n * p->g.H < want_items) {
+    const int64_t s = (total_tok * p->g.H + want_items - 1) / want_items;
+    split = (int)std::max<int64_t>(128, (s + 63) / 64 * 64);
+  }
+  DeviceGuard guard(p->device);
+  fc_status st;
+  if (!p->d_dec_ctr) {
+    st = cuda_check(cudaMalloc(&p->d_dec_ctr, (size_t)kMaxDecode * p->g.H * sizeof(int32_t)),
+                    "cudaMalloc(decode counters)");
+    if (st != FC_OK) return st;
+    st = cuda_check(cudaMemset(p->d_dec_ctr, 0, (size_t)kMaxDecode * p->g.H * sizeof(int32_t)),
+                    "cudaMemset(decode counters)");
+    if (st != FC_OK) return st;
+  }
+  for (int c = 0; c < n; c += kMaxDecode) {
+    DecodeBatch b;
+    memset(&b, 0, sizeof(b));
+    b.n = std::min(kMaxDecode, n - c);
+    b.Hq = num_q_heads;
+    b.layer = layer;
+    b.split_tokens = split;
+    int items = 0;
+    for (int i = 0; i < b.n; ++i) {
+      const int64_t T = p->slots[slot[c + i]].tokens;
+      const int ns = (int)((T + split - 1) / split);
+      b.req[i] = DecodeReq{slot[c + i], (int32_t)T, items, ns, c + i};
+      items += p->g.H * ns;
+    }
+    b.items = items;
+    const int64_t need = (int64_t)items * gq * (p->g.D + 2);
+    if (need > p->dec_ws_floats) {
+      cudaStreamSynchronize((cudaStream_t)stream);
+      cudaFree(p->d_dec_ws);
+      p->d_dec_ws = nullptr;
+      p->dec_ws_floats = 0;
+      st = cuda_check(cudaMalloc(&p->d_dec_ws, need * sizeof(float)), "cudaMalloc(decode workspace)");
+      if (st != FC_OK) return st;
+      p->dec_ws_floats = need;
+    }
+    st = launch_decode_attention(p->g, p->cfg.dtype, p->arena, p->d_table, b, gq, q, out,
+                                 scale_log2, p->d_dec_ws, p->d_dec_ctr, (cudaStream_t)stream);
+    if (st != FC_OK) return st;
   }
   return FC_OK;
 }

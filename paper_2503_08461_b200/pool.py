@@ -298,6 +298,19 @@ class _NativePool:
                                             nat.i64_array(tokens), ctypes.byref(req),
                                             ctypes.byref(avail), self.stream()), req, avail)
 
+    def write_kv(self, layer: int, handle_ids, positions, k, v) -> None:
+        pos = nat.i64_array(positions) if positions is not None else None
+        self._check(self.lib.fc_pool_write_kv(self.ptr, layer, len(handle_ids),
+                                              nat.i64_array(handle_ids), pos,
+                                              ctypes.c_void_p(k.data_ptr()),
+                                              ctypes.c_void_p(v.data_ptr()), self.stream()))
+
+    def decode_attention(self, layer: int, handle_ids, num_q_heads: int, scale: float, q,
+                         out) -> None:
+        self._check(self.lib.fc_pool_decode_attention(
+            self.ptr, layer, len(handle_ids), nat.i64_array(handle_ids), num_q_heads, scale,
+            ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(out.data_ptr()), self.stream()))
+
     def release(self, handle_ids) -> None:
         self._check(self.lib.fc_pool_release_batch(self.ptr, len(handle_ids),
                                                    nat.i64_array(handle_ids), self.stream()))
@@ -636,6 +649,65 @@ class KVCachePool:
         handle.bytes += needed
         self._apply(now, "append", handle.handle_id, needed)
         return handle
+
+    def append_decode_batch(self, handles: Sequence[CacheHandle], token_count: int,
+                            now: float) -> list[CacheHandle]:
+        """``append_decode_tokens(h, token_count, now)`` for every member, in order, as one
+        device call (the per-step loop of engine.py:514-521). Atomic: every member is
+        checked against the remaining capacity before any mutation."""
+        handles = list(handles)
+        if token_count < 1:
+            raise ValueError("token_count must be >= 1")
+        needed = kv_bytes(self.config, token_count)
+        avail = self.available_bytes
+        for h in handles:
+            if h.state is not HandleState.COMPRESSED:
+                raise InvalidState(f"append requires a compressed handle, got {h.state}")
+            if needed > avail:
+                raise CapacityExceeded(needed, avail)
+            avail -= needed
+        if self._native is not None and handles:
+            self._native.append([h.handle_id for h in handles], [token_count] * len(handles))
+        for h in handles:
+            h.spec = replace(h.spec, decode_appended_tokens=h.spec.decode_appended_tokens + token_count)
+            h.bytes += needed
+            self._apply(now, "append", h.handle_id, needed)
+        return handles
+
+    def write_decode_kv(self, handles: Sequence[CacheHandle], layer: int, k, v,
+                        positions: Sequence[int] | None = None) -> None:
+        """Write one token's K and V ([n, Hkv, D] each, pool dtype, CUDA) per handle into
+        layer ``layer`` of its blocks at ``positions`` (default: its last token, the slot
+        ``append_decode_batch`` just added) -- the UpdateKVCache of PAPER.md:255-261."""
+        nv = self._need_native()
+        cfg = self.config
+        want = (len(handles), cfg.num_kv_heads, cfg.head_dim)
+        for t in (k, v):
+            if tuple(t.shape) != want or t.dtype != nv.torch_dtype or t.device != nv.device \
+                    or not t.is_contiguous():
+                raise ValueError(f"k and v must be contiguous {nv.kv_dtype} CUDA tensors {want}")
+        if handles:
+            nv.write_kv(layer, [h.handle_id for h in handles], positions, k, v)
+
+    def decode_attention(self, handles: Sequence[CacheHandle], layer: int, q, out=None,
+                         scale: float | None = None):
+        """softmax(scale * q K^T) V of one query token per handle over every live token of
+        its (compressed + decoded) cache in layer ``layer``: q [n, Hq, D] (pool dtype,
+        CUDA) -> out [n, Hq, D]. Hq = ``num_q_heads``; scale defaults to 1/sqrt(D)."""
+        nv = self._need_native()
+        cfg = self.config
+        want = (len(handles), self.num_q_heads, cfg.head_dim)
+        if tuple(q.shape) != want or q.dtype != nv.torch_dtype or q.device != nv.device \
+                or not q.is_contiguous():
+            raise ValueError(f"q must be a contiguous {nv.kv_dtype} CUDA tensor {want}")
+        if out is None:
+            out = nv.torch.empty_like(q)
+        elif tuple(out.shape) != want or out.dtype != q.dtype or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous {nv.kv_dtype} tensor {want}")
+        if handles:
+            nv.decode_attention(layer, [h.handle_id for h in handles], self.num_q_heads,
+                                0.0 if scale is None else float(scale), q, out)
+        return out
 
     def release(self, handle: CacheHandle, now: float) -> None:
         """Free a cache; legacy mode also drops the retained raw bytes (pool.py:213-224)."""
