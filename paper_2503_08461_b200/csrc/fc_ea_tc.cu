@@ -43,6 +43,7 @@ constexpr int kTileM = 128;
 constexpr int kBRows = 144;                     // 128 Sigma^T rows + mu + 15 zero rows
 constexpr int kSlotCols = 256;                  // TMEM slot stride (N = 144 used)
 constexpr int kSlots = 2;
+constexpr int kMaxChunks = 16;                  // tile rows / smallest block size (8)
 constexpr int kStageBytes = kTileM * kD * 2;    // 32 KB: one K/V tile or half of Sigma (fp32)
 constexpr int kBHalf = kBRows * 128;            // one 64-column slab of B (bytes)
 constexpr int kBBytes = 2 * kBHalf;             // one full B matrix (hi or lo)
@@ -76,16 +77,23 @@ __host__ __device__ inline Smem plan(int bs, int max_T, int max_K) {
 }
 
 // Positions of one segment's stages in the global FIFO ring sequence:
-//   [Sigma(first) x2] then per segment: [K tiles][Sigma(next) x2 if any][V tiles].
+//   [Sigma(first) x2] then per segment: [K tiles][V tiles][Sigma(next) x2 if any].
+// The MMA warp waits only on K-tile positions, so it must never be able to
+// wait on a stage more than one phase ahead of the producer (mbarrier parity
+// waits alias two phases apart). With Sigma(next) LAST, the MMA can only pass
+// b_full after the consumers released every earlier position, so the first
+// K tile it waits on is exactly one phase ahead of its stage's last release.
+// (The old order [K][Sigma(next)][V] let the MMA reach the next K tile while
+// V stages were still in flight: a parity alias fed it a V tile, or hung it.)
 struct SegPos {
-  int k0, sig_next, v0, next;
+  int k0, v0, sig_next, next;
 };
 __device__ __forceinline__ SegPos seg_pos(int start, int ntiles, bool has_next) {
   SegPos s;
   s.k0 = start;
-  s.sig_next = start + ntiles;
-  s.v0 = s.sig_next + (has_next ? 2 : 0);
-  s.next = s.v0 + ntiles;
+  s.v0 = start + ntiles;
+  s.sig_next = s.v0 + ntiles;
+  s.next = s.sig_next + (has_next ? 2 : 0);
   return s;
 }
 
@@ -191,15 +199,24 @@ __global__ void __launch_bounds__(kEaThreads, 1)
         const int nb = (q.T + g.bs - 1) / g.bs, ntiles = (q.T + kTileM - 1) / kTileM;
         const int64_t row_l = ((int64_t)l * g.num_blocks * 2 + kv) * g.H * g.bs + (int64_t)h * g.bs;
         for (int k = 0; k < ntiles; ++k, ++pos) {
+          const int n_chunks = min(chunks, nb - k * chunks);
+          // the tile's block ids: independent loads issued together, before the
+          // stage wait, so their latency hides behind it (one dependent global
+          // round trip per chunk used to serialise the producer)
+          int blk[kMaxChunks];
+#pragma unroll
+          for (int c = 0; c < kMaxChunks; ++c)
+            if (c < n_chunks) blk[c] = __ldg(table + (int64_t)q.slot * g.max_bpr + k * chunks + c);
           unsigned char* dst = acquire(pos);
           uint64_t* bar = &st_full[pos % kStages];
-          const int n_chunks = min(chunks, nb - k * chunks);
           tc::mbar_expect_tx(bar, (uint32_t)(n_chunks * g.bs * kD * 2));
-          for (int c = 0; c < n_chunks; ++c) {
-            const int blk = table[(int64_t)q.slot * g.max_bpr + k * chunks + c];
-            const int64_t row0 = row_l + (int64_t)blk * 2 * g.H * g.bs;
-            tc::tma_load_2d(dst + c * g.bs * 128, &kmap, bar, 0, (int)row0);
-            tc::tma_load_2d(dst + kTileM * 128 + c * g.bs * 128, &kmap, bar, 64, (int)row0);
+#pragma unroll
+          for (int c = 0; c < kMaxChunks; ++c) {
+            if (c < n_chunks) {
+              const int64_t row0 = row_l + (int64_t)blk[c] * 2 * g.H * g.bs;
+              tc::tma_load_2d(dst + c * g.bs * 128, &kmap, bar, 0, (int)row0);
+              tc::tma_load_2d(dst + kTileM * 128 + c * g.bs * 128, &kmap, bar, 64, (int)row0);
+            }
           }
         }
       };
@@ -208,8 +225,8 @@ __global__ void __launch_bounds__(kEaThreads, 1)
         const int lh = item % LH, l = lh / g.H, h = lh % g.H;
         const PressReq q = b.req[item / LH];
         load_tiles(q, l, h, 0);
-        if (item + (int)gridDim.x < n_items) load_sigma(item + gridDim.x);
         load_tiles(q, l, h, 1);
+        if (item + (int)gridDim.x < n_items) load_sigma(item + gridDim.x);
       }
     }
     __syncwarp();
@@ -272,7 +289,12 @@ __global__ void __launch_bounds__(kEaThreads, 1)
     const float inv_sqrt_d = 1.0f / sqrtf((float)kD);
     const float inv_2d = 1.0f / (2.0f * (float)kD);
 
+    // The consumers read ring stages with generic-proxy loads and the producer
+    // refills them with TMA (async proxy): order the reads before the refill
+    // with a proxy fence ahead of the release (without it a fast producer's TMA
+    // overwrote K/Sigma/V rows still being read -- wrong z_t, or a hang).
     auto release_stage = [&](int p) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&st_empty[p % kStages]);
     };
@@ -361,11 +383,6 @@ __global__ void __launch_bounds__(kEaThreads, 1)
         release_stage(p);
         if (t < T_len) atomicAdd(&zt[t], grp == 0 ? fmaf(lin, inv_sqrt_d, acc * inv_2d) : acc * inv_2d);
       }
-      // ---- the next segment's Sigma while the MMA warp idles on B ----
-      if (has_next) {
-        tc::mbar_wait(b_empty, it & 1);
-        convert_sigma(sp.sig_next, item + gridDim.x);
-      }
       Consumers::sync();
       // ---- softmax over t >= n_sink ----
       float m = -INFINITY;
@@ -405,6 +422,11 @@ __global__ void __launch_bounds__(kEaThreads, 1)
         release_stage(p);
         const int t = k * kTileM + row;
         if (half == 0 && t < T_len && t >= ns) zt[t] = expf(zt[t] - m) * inv_z * sqrtf(sq);
+      }
+      // ---- the next segment's Sigma (last in the ring order, see SegPos) ----
+      if (has_next) {
+        tc::mbar_wait(b_empty, it & 1);
+        convert_sigma(sp.sig_next, item + gridDim.x);
       }
       Consumers::sync();
       for (int t = ct; t < ns && t < T_len; t += kThreads) zt[t] = INFINITY;
