@@ -35,14 +35,33 @@
 
 namespace fc {
 
+#ifdef FC_TRACE
+// Debug build only (make trace): per-CTA, per-segment %globaltimer stamps.
+__device__ unsigned long long g_fc_trace_ea[148 * 64 * 8];
+__device__ __forceinline__ void ea_stamp(int it, int slot) {
+  if (it < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_fc_trace_ea[(blockIdx.x * 64 + it) * 8 + slot] = t;
+  }
+}
+#define EA_STAMP(it, slot) ea_stamp(it, slot)
+#else
+#define EA_STAMP(it, slot) ((void)0)
+#endif
+
 namespace ea {
 
 constexpr int kD = 128;
 constexpr int kStages = 3;
 constexpr int kTileM = 128;
 constexpr int kBRows = 144;                     // 128 Sigma^T rows + mu + 15 zero rows
-constexpr int kSlotCols = 256;                  // TMEM slot stride (N = 144 used)
-constexpr int kSlots = 2;
+#ifndef FC_EA_SLOTS
+#define FC_EA_SLOTS 3
+#endif
+constexpr int kSlots = FC_EA_SLOTS;              // TMEM ring depth (MMA runs kSlots tiles ahead)
+constexpr int kSlotCols = kSlots == 2 ? 256 : 160;  // slot stride (N = 144 used)
+constexpr int kTmemCols = 512;                  // power-of-two allocation >= kSlots * kSlotCols
 constexpr int kMaxChunks = 16;                  // tile rows / smallest block size (8)
 constexpr int kStageBytes = kTileM * kD * 2;    // 32 KB: one K/V tile or half of Sigma (fp32)
 constexpr int kBHalf = kBRows * 128;            // one 64-column slab of B (bytes)
@@ -168,7 +187,7 @@ __global__ void __launch_bounds__(kEaThreads, 1)
     *reinterpret_cast<uint4*>(bmat + mat * kBBytes + half * kBHalf + (n >> 3) * 1024 + (n & 7) * 128 + (c << 4)) =
         make_uint4(0, 0, 0, 0);
   }
-  if (warp == 1) tc::tmem_alloc(&s_tmem, kSlots * kSlotCols);
+  if (warp == 1) tc::tmem_alloc(&s_tmem, kTmemCols);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -272,12 +291,16 @@ __global__ void __launch_bounds__(kEaThreads, 1)
     for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
       const int jb = it & 1;
       tc::mbar_wait(&job_full[jb], (it >> 1) & 1);
+      if (Compactors::tid() == 0) EA_STAMP(it, 6);
       const Job job = s_job[jb];
       char* seg = arena + g.seg_base(job.l, 0, job.h);
       compact_rows<kD * 2, Compactors, 8>(seg, g, ctab + jb * nb_stride, ctab + jb * nb_stride,
                                           idxbuf + jb * k_stride, job.K, job.first_moved);
       Compactors::sync();
-      if (Compactors::tid() == 0) tc::mbar_arrive(&job_empty[jb]);
+      if (Compactors::tid() == 0) {
+        EA_STAMP(it, 7);
+        tc::mbar_arrive(&job_empty[jb]);
+      }
     }
   } else {
     // ================= consumers =================
@@ -345,7 +368,10 @@ __global__ void __launch_bounds__(kEaThreads, 1)
       const SegPos sp = seg_pos(pos, ntiles, has_next);
       const int jb = it & 1;
       for (int t = ct; t < T_len; t += kThreads) zt[t] = 0.f;
-      if (ct == 0) ss.first_drop = INT_MAX;
+      if (ct == 0) {
+        ss.first_drop = INT_MAX;
+        EA_STAMP(it, 0);
+      }
       Consumers::sync();
       // ---- z_t from TMEM (Y = K.B^T) and the K rows still in SMEM ----
       for (int k = 0; k < ntiles; ++k, ++gt) {
@@ -384,6 +410,7 @@ __global__ void __launch_bounds__(kEaThreads, 1)
         if (t < T_len) atomicAdd(&zt[t], grp == 0 ? fmaf(lin, inv_sqrt_d, acc * inv_2d) : acc * inv_2d);
       }
       Consumers::sync();
+      if (ct == 0) EA_STAMP(it, 1);
       // ---- softmax over t >= n_sink ----
       float m = -INFINITY;
       for (int t = ns + ct; t < T_len; t += kThreads) m = fmaxf(m, zt[t]);
@@ -403,6 +430,7 @@ __global__ void __launch_bounds__(kEaThreads, 1)
       z = 0.f;
       for (int w = 0; w < kWarps; ++w) z += ss.red[w];
       const float inv_z = 1.0f / z;
+      if (ct == 0) EA_STAMP(it, 2);
       // ---- V tiles: s_t = p_t * ||V_t|| (two lanes per row) ----
       for (int k = 0; k < ntiles; ++k) {
         const int p = sp.v0 + k;
@@ -423,12 +451,14 @@ __global__ void __launch_bounds__(kEaThreads, 1)
         const int t = k * kTileM + row;
         if (half == 0 && t < T_len && t >= ns) zt[t] = expf(zt[t] - m) * inv_z * sqrtf(sq);
       }
+      if (ct == 0) EA_STAMP(it, 3);
       // ---- the next segment's Sigma (last in the ring order, see SegPos) ----
       if (has_next) {
         tc::mbar_wait(b_empty, it & 1);
         convert_sigma(sp.sig_next, item + gridDim.x);
       }
       Consumers::sync();
+      if (ct == 0) EA_STAMP(it, 4);
       for (int t = ct; t < ns && t < T_len; t += kThreads) zt[t] = INFINITY;
       Consumers::sync();
       if (out.scores) {
@@ -454,13 +484,16 @@ __global__ void __launch_bounds__(kEaThreads, 1)
       }
       if (ct == 0) s_job[jb] = Job{l, h, K, min(ss.first_drop, K)};
       Consumers::sync();
-      if (ct == 0) tc::mbar_arrive(&job_full[jb]);
+      if (ct == 0) {
+        EA_STAMP(it, 5);
+        tc::mbar_arrive(&job_full[jb]);
+      }
       pos = sp.next;
     }
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tmem, kSlots * kSlotCols);
+  if (warp == 1) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
 // ---------------------------------------------------------------------------
@@ -504,3 +537,9 @@ fc_status launch_ea_tc(const Geom& g, char* arena, const int32_t* table, const P
 }
 
 }  // namespace fc
+
+#ifdef FC_TRACE
+extern "C" FC_API fc_status fc_debug_trace_read_ea(void* host, uint64_t bytes) {
+  return fc::cuda_check(cudaMemcpyFromSymbol(host, fc::g_fc_trace_ea, bytes), "trace read");
+}
+#endif

@@ -1,5 +1,6 @@
 #!/bin/bash
-for lib in libfastcache.so libfc_FC_EA_SLEEP.so libfc_FC_EA_PROXY_FENCE.so libfc_FC_EA_IDS_AFTER.so; do
-echo "$lib: $(FASTCACHE_LIB=$PWD/paper_2503_08461_b200/_lib/$lib timeout 300 python -m pytest tests/test_gpu_press.py -q -k expected_attention 2>&1 | tail -1)"
+L=$PWD/paper_2503_08461_b200/_lib
+timeout 300 python -m pytest tests/test_gpu_press.py -q -k expected_attention 2>&1 | tail -1
+for lib in libfastcache.so libfc_slots2.so; do
+FASTCACHE_LIB=$L/$lib timeout 300 python bench.py --config c4w --steps 5 --warmup 3 --e2e-steps 0 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); print('$lib', d['ms_per_step'], d['roofline']['frac'])"
 done
-FASTCACHE_LIB=$PWD/paper_2503_08461_b200/_lib/libfastcache.so timeout 300 python -m pytest tests/test_gpu_press.py -q -k expected_attention 2>&1 | grep -B2 "Error" | head -30

@@ -32,9 +32,11 @@ t0 = tr[tr > 0].min()
 d = (tr[:, 2:60] - t0) / 1e3
 d[tr[:, 2:60] == 0] = np.nan
 m = lambda x: float(np.nanmean(x))
-print("z epilogue %.1f  sigma convert %.1f  softmax %.1f  V norms %.1f  select+handoff %.1f us" % (
+d = (tr[:, 2:60] - t0) / 1e3
+d[tr[:, 2:60] == 0] = np.nan
+print("z epilogue %.1f  softmax %.1f  V norms %.1f  sigma convert %.1f  select+handoff %.1f us" % (
     m(d[:, :, 1] - d[:, :, 0]), m(d[:, :, 2] - d[:, :, 1]), m(d[:, :, 3] - d[:, :, 2]),
     m(d[:, :, 4] - d[:, :, 3]), m(d[:, :, 5] - d[:, :, 4])))
-print("consumer period %.1f us, compactor busy %.1f us" % (
-    m(np.diff(d[:, :, 5], axis=1)), m(d[:, :, 7] - d[:, :, 6])))
+print("consumer period %.1f us, compactor busy %.1f us, compactor period %.1f us" % (
+    m(np.diff(d[:, :, 5], axis=1)), m(d[:, :, 7] - d[:, :, 6]), m(np.diff(d[:, :, 6], axis=1))))
 print("consumer idle before segment (wait for next start) %.1f us" % m(d[:, 1:, 0] - d[:, :-1, 5]))
