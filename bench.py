@@ -624,7 +624,32 @@ def cpu_reference(args, cfg, dtype, specs, comp, reps: int | None = None):
               f"shared{note}")
     return {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["workers"], "kind": "port",
             "sample": sample, "seconds": r["seconds"],
-            "cpu_model": _cpu_model()}
+            "cpu_model": _cpu_model(),
+            "literal_reference_path": literal_reference_path(cfg, kv, segs, comp)}
+
+
+def literal_reference_path(cfg, kv, segs, comp, layers: int = 2):
+    """SURVEY.md §8(d) CPU path 1: the reference's own tensor compressor -- compress_tensor
+    (MEAN_POOL, kv.py:211-239, restated in oracle/chunk.py) on every (layer, K|V, head,
+    modality segment), one thread, timed on ``layers`` layers and extrapolated to L."""
+    import numpy as np
+
+    from oracle import chunk
+
+    t0 = time.perf_counter()
+    for layer in range(layers):
+        for kvi in range(2):
+            for head in range(cfg.num_kv_heads):
+                start = 0
+                for n in segs:
+                    chunk.compress_tensor(kv[layer, kvi, head, start:start + n], comp.factor, "meanpool")
+                    start += n
+    secs = (time.perf_counter() - t0) * cfg.num_layers / layers
+    tokens = kv.shape[3]
+    return {"value": tokens / secs, "unit": "tokens/s", "cores": 1, "kind": "port",
+            "sample": f"1 request x {layers} of {cfg.num_layers} layers x {cfg.num_kv_heads} heads x "
+                      f"K|V x segments {list(segs)}, compress_tensor MEAN_POOL factor {comp.factor}, "
+                      "extrapolated linearly to all layers"}
 
 
 def _cpu_model():

@@ -50,7 +50,10 @@ __device__ __forceinline__ void trace_stamp(int it, int slot) {
 #define FC_STAMP(it, slot) ((void)0)
 #endif
 
-constexpr int kTcStages = 3;
+#ifndef FC_SNAP_STAGES
+#define FC_SNAP_STAGES 3
+#endif
+constexpr int kTcStages = FC_SNAP_STAGES;
 constexpr int kTileM = 128;
 constexpr int kSlots = 16;                      // TMEM ring: 16 x 32 fp32 columns
 constexpr int kWin = 32;                        // window queries (UMMA N)
