@@ -262,4 +262,75 @@ __device__ __forceinline__ void compact_rows(char* __restrict__ seg, const Geom&
   }
 }
 
+
+// Same contract as compact_rows, but the rows travel through an SMEM ring of
+// kNBuf chunks with cp.async (LDGSTS), so kNBuf - 1 chunks of loads are in
+// flight without holding registers (the register version keeps one chunk
+// ahead). Chunk c = kRanks ranks x {K, V}. Iteration c: wait for chunk c,
+// barrier, issue the loads of chunk c + kNBuf - 1 into the buffer chunk c - 1
+// used, then store chunk c from SMEM. In place: chunk c stores ranks
+// [cW, (c+1)W) only after every load of chunks <= c completed (the barrier),
+// and every load still in flight reads positions >= (c+1)W.
+template <int kRowBytes, class G, int kRanks, int kNBuf>
+struct AsyncCompactor {
+  static constexpr int kVecs = kRowBytes / 16;
+  static constexpr int kItems = kRanks * 2 * kVecs / kThreads;  // 16-B pieces per thread
+  static_assert(kItems * kThreads == kRanks * 2 * kVecs, "chunk must split evenly over the group");
+  static constexpr int kChunkBytes = kRanks * 2 * kRowBytes;
+  static constexpr int kSmemBytes = kNBuf * kChunkBytes;
+};
+
+template <int kRowBytes, class G, int kRanks = 32, int kNBuf = 4>
+__device__ __forceinline__ void compact_rows_async(char* __restrict__ seg, const Geom& g,
+                                                   const int32_t* s_src, const int32_t* s_dst,
+                                                   const int32_t* idx, int K, int j_start,
+                                                   unsigned char* smem) {
+  using A = AsyncCompactor<kRowBytes, G, kRanks, kNBuf>;
+  constexpr int kVecs = A::kVecs;
+  if (j_start >= K) return;
+  const int64_t kv_off = (int64_t)g.H * g.bs * kRowBytes;
+  const int nchunks = (K - j_start + kRanks - 1) / kRanks;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  auto issue = [&](int c) {
+    if (c < nchunks) {
+      const uint32_t buf = sbase + (uint32_t)((c % kNBuf) * A::kChunkBytes);
+#pragma unroll
+      for (int it = 0; it < A::kItems; ++it) {
+        const int v = it * kThreads + G::tid();
+        const int rank = v / (2 * kVecs), rem = v % (2 * kVecs);
+        const int kv = rem / kVecs, vec = rem % kVecs;
+        const int j = j_start + c * kRanks + rank;
+        if (j < K) {
+          const int src = idx[j];
+          const char* gp = seg + kv * kv_off + (int64_t)s_src[src >> g.bs_shift] * g.block_stride +
+                           (int64_t)(src & (g.bs - 1)) * kRowBytes + vec * 16;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(buf + v * 16), "l"(gp)
+                       : "memory");
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");  // uniform group count, even if empty
+  };
+#pragma unroll
+  for (int c = 0; c < kNBuf - 1; ++c) issue(c);
+  for (int c = 0; c < nchunks; ++c) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kNBuf - 2) : "memory");
+    G::sync();  // chunk c landed everywhere; chunk c-1's buffer fully read
+    issue(c + kNBuf - 1);
+    const unsigned char* buf = smem + (c % kNBuf) * A::kChunkBytes;
+#pragma unroll
+    for (int it = 0; it < A::kItems; ++it) {
+      const int v = it * kThreads + G::tid();
+      const int rank = v / (2 * kVecs), rem = v % (2 * kVecs);
+      const int kv = rem / kVecs, vec = rem % kVecs;
+      const int j = j_start + c * kRanks + rank;
+      if (j < K)
+        st_stream(seg + kv * kv_off + (int64_t)s_dst[j >> g.bs_shift] * g.block_stride +
+                      (int64_t)(j & (g.bs - 1)) * kRowBytes + vec * 16,
+                  *reinterpret_cast<const uint4*>(buf + v * 16));
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 }  // namespace fc

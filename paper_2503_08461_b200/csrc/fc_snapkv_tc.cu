@@ -67,9 +67,20 @@ struct CompactJob {  // consumer -> compactor hand-off of one segment
   int32_t l, h, K, first_moved;
 };
 
+#ifndef FC_SNAP_ASYNC_COMPACT
+#define FC_SNAP_ASYNC_COMPACT 1
+#endif
+#ifndef FC_SNAP_CRANKS
+#define FC_SNAP_CRANKS 32
+#endif
+#ifndef FC_SNAP_CBUFS
+#define FC_SNAP_CBUFS 4
+#endif
+
 struct TcSmem {
   int tile_bytes, q_bytes, max_nb;
-  int off_stage, off_q, off_ptab, off_ctab, off_idx, off_sc, off_s1, off_bar, total;
+  int off_stage, off_q, off_ptab, off_ctab, off_idx, off_sc, off_s1, off_bar, off_cbuf, total;
+  bool async_compact;
 };
 
 __host__ __device__ inline TcSmem tc_smem_plan(int D, int bs, int max_T) {
@@ -85,7 +96,12 @@ __host__ __device__ inline TcSmem tc_smem_plan(int D, int bs, int max_T) {
   p.off_sc = p.off_idx + 2 * ((max_T * 4 + 15) & ~15);
   p.off_s1 = p.off_sc + ((max_T * 4 + 15) & ~15);
   p.off_bar = p.off_s1 + 2 * ((max_T * 4 + 15) & ~15);
+  p.off_cbuf = p.off_bar + (((2 * kTcStages + 8 + 2 * kSlots) * 8 + 127) & ~127);
   p.total = p.off_bar + (2 * kTcStages + 8 + 2 * kSlots) * 8 + 1024;
+  // the compactors' cp.async ring (D * 2-byte rows, 4 x 32-rank chunks) when it fits
+  const int cbuf = FC_SNAP_CBUFS * FC_SNAP_CRANKS * 2 * D * 2;
+  p.async_compact = FC_SNAP_ASYNC_COMPACT && p.off_cbuf + cbuf + 1024 <= 227 * 1024;
+  if (p.async_compact) p.total = p.off_cbuf + cbuf + 1024;
   return p;
 }
 
@@ -225,9 +241,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const CompactJob job = s_job[jb];
       char* seg = arena + g.seg_base(job.l, 0, job.h);
 #ifndef FC_NO_COMPACT
-      compact_rows<D * (int)sizeof(T), Compactors, 8>(seg, g, ctab + jb * nb_stride,
-                                                   ctab + jb * nb_stride, idxbuf + jb * t_stride,
-                                                   job.K, job.first_moved);
+      if (plan.async_compact)
+        compact_rows_async<D * (int)sizeof(T), Compactors, FC_SNAP_CRANKS, FC_SNAP_CBUFS>(
+            seg, g, ctab + jb * nb_stride, ctab + jb * nb_stride, idxbuf + jb * t_stride, job.K,
+            job.first_moved, smem + plan.off_cbuf);
+      else
+        compact_rows<D * (int)sizeof(T), Compactors, 8>(seg, g, ctab + jb * nb_stride,
+                                                     ctab + jb * nb_stride, idxbuf + jb * t_stride,
+                                                     job.K, job.first_moved);
 #endif
       Compactors::sync();
       if (Compactors::tid() == 0) {
