@@ -345,23 +345,30 @@ __device__ void score_ea(const char* __restrict__ seg, const Geom& g, const int3
 // ---------------------------------------------------------------------------
 // the fused kernel
 // ---------------------------------------------------------------------------
+#ifndef FC_KNORM_ASYNC  // Knorm compaction through a cp.async SMEM ring (fc_select.cuh)
+#define FC_KNORM_ASYNC 1
+#endif
+constexpr int kKnRanks = 16, kKnBufs = 4;
+
 struct SmemPlan {
   int nb;          // table entries per table
   int tab_bytes;   // both tables
   int sc_bytes;    // scores
   int scratch_bytes;
-  __host__ __device__ int total() const { return tab_bytes + sc_bytes + scratch_bytes; }
+  int cbuf_bytes;  // Knorm: cp.async compaction ring
+  __host__ __device__ int total() const { return tab_bytes + sc_bytes + scratch_bytes + cbuf_bytes; }
 };
 
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
 __host__ __device__ inline SmemPlan smem_plan(int kind, int max_T, int bs, int D, int window,
-                                              bool in_place) {
+                                              bool in_place, int row_bytes = 256) {
   SmemPlan p;
   p.nb = (max_T + bs - 1) / bs;
   p.tab_bytes = align16(p.nb * 4) * (in_place ? 1 : 2);
   p.sc_bytes = align16(max_T * 4);
   p.scratch_bytes = 0;
+  p.cbuf_bytes = (FC_KNORM_ASYNC && kind == FC_PRESS_KNORM) ? kKnBufs * kKnRanks * 2 * row_bytes : 0;
   if (kind == FC_PRESS_SNAPKV)
     p.scratch_bytes = align16((window * (D + 1) + 32 * (D + 1) + ((max_T + 3) & ~3) + 2 * window) * 4);
   else if (kind == FC_PRESS_EXPECTED_ATTENTION)
@@ -378,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, KIND == FC_PRESS_KNORM ? 4 : 2)
                  int64_t ws_per_cta, int n_items) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SelectScratch ss;
-  const SmemPlan plan = smem_plan(KIND, b.max_T, g.bs, D, pp.window, b.in_place != 0);
+  const SmemPlan plan = smem_plan(KIND, b.max_T, g.bs, D, pp.window, b.in_place != 0, D * (int)sizeof(T));
   int32_t* s_src = reinterpret_cast<int32_t*>(smem);
   int32_t* s_dst = b.in_place ? s_src : s_src + plan.tab_bytes / 8;
   float* sc = reinterpret_cast<float*>(smem + plan.tab_bytes);
@@ -439,7 +446,12 @@ __global__ void __launch_bounds__(kThreads, KIND == FC_PRESS_KNORM ? 4 : 2)
     const int first_moved = b.in_place ? min(ss.first_drop, K) : 0;
 
     // ---- phase 3: compact K and V rows into the destination blocks ----
-    compact_rows<D * (int)sizeof(T)>(seg, g, s_src, s_dst, idx, K, first_moved);
+    if (FC_KNORM_ASYNC && KIND == FC_PRESS_KNORM)
+      compact_rows_async<D * (int)sizeof(T), CtaGroup, kKnRanks, kKnBufs>(
+          seg, g, s_src, s_dst, idx, K, first_moved,
+          smem + plan.tab_bytes + plan.sc_bytes + plan.scratch_bytes);
+    else
+      compact_rows<D * (int)sizeof(T)>(seg, g, s_src, s_dst, idx, K, first_moved);
   }
 }
 
@@ -577,7 +589,7 @@ static fc_status launch_one(const Geom& g, char* arena, const int32_t* src, int3
     if (ea_tc_supported(g, Elem<T>::kDtype, pp, b.max_T, max_K))
       return launch_ea_tc(g, arena, src, b, pp, in, out, max_K, stream);
   }
-  const SmemPlan plan = smem_plan(KIND, b.max_T, g.bs, D, pp.window, b.in_place != 0);
+  const SmemPlan plan = smem_plan(KIND, b.max_T, g.bs, D, pp.window, b.in_place != 0, D * (int)sizeof(T));
   const int smem = plan.total();
   if (smem > 220 * 1024)
     return set_error(FC_ERR_UNSUPPORTED, "request of %d tokens exceeds the SMEM budget", b.max_T);
