@@ -277,6 +277,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (ct == 0) ss.first_drop = INT_MAX;
 
       float acc[16];
+      // s1 = the window mean of both query groups (pass 3 adds into it)
+      for (int t = ct; t < T_len; t += kThreads) s1[t] = 0.f;
       // pass 1: per-query max over all tokens
 #pragma unroll
       for (int j = 0; j < 16; ++j) acc[j] = -INFINITY;
@@ -292,13 +294,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           if (t < T_len && t <= T_len - kWin + grp * 16 + j) acc[j] = fmaxf(acc[j], v[j] * scale);
       }
       if (ct == 0) FC_STAMP(it, 3);
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) acc[j] = fmaxf(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], off));
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (lane == j) s_red[cw][j] = acc[j];
+      {
+        const float r = tc::warp_reduce16(acc, lane, [](float a, float b) { return fmaxf(a, b); });
+        if ((lane & 1) == 0) s_red[cw][lane >> 1] = r;
+      }
       Consumers::sync();
       if (ct < kWin) {
         const int gg = ct >> 4, jj = ct & 15;
@@ -329,13 +328,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       tc::tmem_store_wait();
       if (ct == 0) FC_STAMP(it, 9);
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (lane == j) s_red[cw][j] = acc[j];
+      {
+        const float r = tc::warp_reduce16(acc, lane, [](float a, float b) { return a + b; });
+        if ((lane & 1) == 0) s_red[cw][lane >> 1] = r;
+      }
       Consumers::sync();
       if (ct < kWin) {
         const int gg = ct >> 4, jj = ct & 15;
@@ -358,10 +354,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
         const int t = k * kTileM + row;
         if (t < n_keep) {
-          float s = 0.f;
+          float sum = 0.f;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) s = fmaf(v[j], zj[j], s);   // masked entries are 0
-          s1[grp * s1_stride + t] = s * (1.0f / (float)kWin);
+          for (int j = 0; j < 16; ++j) sum = fmaf(v[j], zj[j], sum);   // masked entries are 0
+          atomicAdd(&s1[t], sum * (1.0f / (float)kWin));   // two addends onto 0: order-free
         }
       }
       gtile += ntiles;
@@ -375,7 +371,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (t < n_keep) {
           float a = 0.f;
           const int u0 = max(0, t - half), u1 = min(n_keep - 1, t + half);
-          for (int u = u0; u <= u1; ++u) a += s1[u] + s1[s1_stride + u];
+          for (int u = u0; u <= u1; ++u) a += s1[u];
           v = a * inv_p;
         }
         sc[t] = v;
