@@ -133,7 +133,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   int32_t* idxbuf = reinterpret_cast<int32_t*>(smem + plan.off_idx);  // [2][t_stride]
   __shared__ CompactJob s_job[2];
   float* sc = reinterpret_cast<float*>(smem + plan.off_sc);
-  float* s1 = reinterpret_cast<float*>(smem + plan.off_s1);  // [2][max_T]
+  // window means, front-padded with 8 zeros so the pooling window needs no bounds
+  // (the plan reserves 2 * max_T floats; one padded array uses max_T + 8)
+  float* s1 = reinterpret_cast<float*>(smem + plan.off_s1) + 8;
   const int s1_stride = ((b.max_T * 4 + 15) & ~15) / 4;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + plan.off_bar);
   uint64_t* st_full = bars;
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
       float acc[16];
       // s1 = the window mean of both query groups (pass 3 adds into it)
-      for (int t = ct; t < T_len; t += kThreads) s1[t] = 0.f;
+      for (int t = ct - 8; t < T_len; t += kThreads) s1[t] = 0.f;
       // pass 1: per-query max over all tokens
 #pragma unroll
       for (int j = 0; j < 16; ++j) acc[j] = -INFINITY;
@@ -366,15 +368,30 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // avg-pool (zero pad, count_include_pad), forced window
       const int half = pp.pool_kernel / 2;
       const float inv_p = 1.0f / (float)pp.pool_kernel;
-      for (int t = ct; t < T_len; t += kThreads) {
-        float v = INFINITY;
-        if (t < n_keep) {
-          float a = 0.f;
-          const int u0 = max(0, t - half), u1 = min(n_keep - 1, t + half);
-          for (int u = u0; u <= u1; ++u) a += s1[u];
-          v = a * inv_p;
+      if (pp.pool_kernel == 7) {
+        // s1 is 0 on [-8, 0) and on [n_keep, T_len) (T_len = n_keep + 32), so the
+        // fixed 7-term window adds exact zeros where the generic loop stops early
+        for (int t = ct; t < T_len; t += kThreads) {
+          float v = INFINITY;
+          if (t < n_keep) {
+            float a = 0.f;
+#pragma unroll
+            for (int u = -3; u <= 3; ++u) a += s1[t + u];
+            v = a * inv_p;
+          }
+          sc[t] = v;
         }
-        sc[t] = v;
+      } else {
+        for (int t = ct; t < T_len; t += kThreads) {
+          float v = INFINITY;
+          if (t < n_keep) {
+            float a = 0.f;
+            const int u0 = max(0, t - half), u1 = min(n_keep - 1, t + half);
+            for (int u = u0; u <= u1; ++u) a += s1[u];
+            v = a * inv_p;
+          }
+          sc[t] = v;
+        }
       }
       Consumers::sync();
       if (out.scores) {
