@@ -29,7 +29,7 @@ struct NamedGroup {
 constexpr int kRadixBins = 256;  // 8-bit digits, 4 passes
 
 struct SelectScratch {
-  uint32_t hist[kRadixBins];
+  uint32_t hist[2][kRadixBins];   // double-buffered: pass p counts into hist[p & 1]
   int32_t warp_tot[kWarps];
   uint32_t emit_tot[2][kWarps];   // double-buffered packed (gt | eq << 16) warp counts
   int32_t sel_bin;
@@ -79,26 +79,30 @@ __device__ void select_emit(const uint32_t* keys, int n, int K, int32_t* out, in
   }
   uint32_t prefix = 0, mask = 0;
   int krem = K;
+  for (int i = tid; i < kRadixBins; i += kThreads) s.hist[0][i] = 0;
+  G::sync();
 #pragma unroll 1
   for (int pass = 0; pass < 4; ++pass) {
     const int shift = 24 - 8 * pass;
-    for (int i = tid; i < kRadixBins; i += kThreads) s.hist[i] = 0;
-    G::sync();
+    uint32_t* hist = s.hist[pass & 1];
     for (int base = 0; base < n; base += kThreads) {
       const int i = base + tid;
       if (i < n) {
         const uint32_t k = keys[i];
-        if ((k & mask) == prefix) atomicAdd(&s.hist[(k >> shift) & 255u], 1u);
+        if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
       }
     }
     G::sync();
-    if (tid < 32) {
+    if (tid >= 32) {
+      // the next pass's histogram is cleared while warp 0 scans this one
+      for (int i = tid - 32; i < kRadixBins; i += kThreads - 32) s.hist[(pass + 1) & 1][i] = 0;
+    } else {
       constexpr int per = kRadixBins / 32;  // 8 bins per lane, lane 31 owns the top
       uint32_t c[per];
       uint32_t local = 0;
 #pragma unroll
       for (int b = 0; b < per; ++b) {
-        c[b] = s.hist[lane * per + b];
+        c[b] = hist[lane * per + b];
         local += c[b];
       }
       uint32_t incl = local;  // sum over lanes >= lane

@@ -368,6 +368,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // avg-pool (zero pad, count_include_pad), forced window
       const int half = pp.pool_kernel / 2;
       const float inv_p = 1.0f / (float)pp.pool_kernel;
+      // scores -> order-preserving keys (and the optional score output) in the same pass
+      uint32_t* keys = reinterpret_cast<uint32_t*>(sc);
+      float* so = out.scores ? out.scores + q.score_off + (int64_t)lh * T_len : nullptr;
       if (pp.pool_kernel == 7) {
         // s1 is 0 on [-8, 0) and on [n_keep, T_len) (T_len = n_keep + 32), so the
         // fixed 7-term window adds exact zeros where the generic loop stops early
@@ -379,7 +382,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (int u = -3; u <= 3; ++u) a += s1[t + u];
             v = a * inv_p;
           }
-          sc[t] = v;
+          if (so) so[t] = v;
+          keys[t] = float_key(v);
         }
       } else {
         for (int t = ct; t < T_len; t += kThreads) {
@@ -390,16 +394,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (int u = u0; u <= u1; ++u) a += s1[u];
             v = a * inv_p;
           }
-          sc[t] = v;
+          if (so) so[t] = v;
+          keys[t] = float_key(v);
         }
       }
-      Consumers::sync();
-      if (out.scores) {
-        float* so = out.scores + q.score_off + (int64_t)lh * T_len;
-        for (int t = ct; t < T_len; t += kThreads) so[t] = sc[t];
-      }
-      uint32_t* keys = reinterpret_cast<uint32_t*>(sc);
-      for (int t = ct; t < T_len; t += kThreads) keys[t] = float_key(sc[t]);
       Consumers::sync();
       if (ct == 0) FC_STAMP(it, 12);
       // hand the kept list to the compactors (double-buffered)
