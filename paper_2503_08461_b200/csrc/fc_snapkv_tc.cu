@@ -291,9 +291,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         float v[16];
         tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
         const int t = k * kTileM + row;
+        if (t <= T_len - kWin) {   // below the window: no causal mask
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (t < T_len && t <= T_len - kWin + grp * 16 + j) acc[j] = fmaxf(acc[j], v[j] * scale);
+          for (int j = 0; j < 16; ++j) acc[j] = fmaxf(acc[j], v[j] * scale);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (t < T_len && t <= T_len - kWin + grp * 16 + j) acc[j] = fmaxf(acc[j], v[j] * scale);
+        }
       }
       if (ct == 0) FC_STAMP(it, 3);
       {
@@ -320,11 +325,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         float v[16];
         tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
         const int t = k * kTileM + row;
+        if (t <= T_len - kWin) {   // below the window: no causal mask
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float e = (t < T_len && t <= T_len - kWin + grp * 16 + j) ? tc::ex2(fmaf(v[j], scale, -mj[j])) : 0.f;
-          acc[j] += e;
-          v[j] = e;
+          for (int j = 0; j < 16; ++j) {
+            v[j] = tc::ex2(fmaf(v[j], scale, -mj[j]));
+            acc[j] += v[j];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float e = (t < T_len && t <= T_len - kWin + grp * 16 + j) ? tc::ex2(fmaf(v[j], scale, -mj[j])) : 0.f;
+            acc[j] += e;
+            v[j] = e;
+          }
         }
         tc::tmem_st_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);   // exps replace the logits
       }
