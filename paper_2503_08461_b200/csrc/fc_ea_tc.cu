@@ -442,7 +442,9 @@ __global__ void __launch_bounds__(kEaThreads, 1)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           float vx[8];
-          unpack16<__half>(*reinterpret_cast<const uint4*>(vrow + (c << 4)), vx);
+          // physical chunk c ^ (row & 7): the 128-B swizzle spreads the 16 rows of a warp
+          // over all 32 banks (unswizzled offsets put every lane on the same 4 banks)
+          unpack16<__half>(*reinterpret_cast<const uint4*>(vrow + ((c ^ (row & 7)) << 4)), vx);
 #pragma unroll
           for (int e = 0; e < 8; ++e) sq = fmaf(vx[e], vx[e], sq);
         }
