@@ -85,6 +85,7 @@ __device__ void select_emit(const uint32_t* keys, int n, int K, int32_t* out, in
   for (int pass = 0; pass < 4; ++pass) {
     const int shift = 24 - 8 * pass;
     uint32_t* hist = s.hist[pass & 1];
+#pragma unroll 4
     for (int base = 0; base < n; base += kThreads) {
       const int i = base + tid;
       if (i < n) {
@@ -132,36 +133,56 @@ __device__ void select_emit(const uint32_t* keys, int n, int K, int32_t* out, in
   }
   const uint32_t tau = prefix;
   const int need = krem;
+  // Emission in super-tiles of kEmitR x 256 keys (warp w owns kEmitR x 32
+  // consecutive keys, one ballot per 32): one barrier per super-tile.
+  constexpr int kEmitR = 4;
   int run_gt = 0, run_eq = 0, buf = 0;
   bool drop_found = false;
-  for (int base = 0; base < n; base += kThreads, buf ^= 1) {
-    const int i = base + tid;
-    const bool valid = i < n;
-    const uint32_t k = valid ? keys[i] : 0u;
-    const bool gt = valid && k > tau, eq = valid && k == tau;
-    const unsigned bg = __ballot_sync(0xffffffffu, gt), be = __ballot_sync(0xffffffffu, eq);
-    if (lane == 0) s.emit_tot[buf][warp] = (uint32_t)__popc(bg) | ((uint32_t)__popc(be) << 16);
+  for (int base = 0; base < n; base += kThreads * kEmitR, buf ^= 1) {
+    const int wbase = base + warp * 32 * kEmitR;
+    unsigned bg[kEmitR], be[kEmitR];
+    int cg = 0, ce = 0;
+#pragma unroll
+    for (int r = 0; r < kEmitR; ++r) {
+      const int i = wbase + r * 32 + lane;
+      const bool valid = i < n;
+      const uint32_t k = valid ? keys[i] : 0u;
+      bg[r] = __ballot_sync(0xffffffffu, valid && k > tau);
+      be[r] = __ballot_sync(0xffffffffu, valid && k == tau);
+      cg += __popc(bg[r]);
+      ce += __popc(be[r]);
+    }
+    if (lane == 0) s.emit_tot[buf][warp] = (uint32_t)cg | ((uint32_t)ce << 16);
     G::sync();
     int g_before = 0, e_before = 0, g_tot = 0, e_tot = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
       const uint32_t c = s.emit_tot[buf][w];
-      const int cg = (int)(c & 0xFFFFu), ce = (int)(c >> 16);
-      g_before += w < warp ? cg : 0;
-      e_before += w < warp ? ce : 0;
-      g_tot += cg;
-      e_tot += ce;
+      const int wg = (int)(c & 0xFFFFu), we = (int)(c >> 16);
+      g_before += w < warp ? wg : 0;
+      e_before += w < warp ? we : 0;
+      g_tot += wg;
+      e_tot += we;
     }
-    const int G_i = run_gt + g_before + __popc(bg & lt_mask);
-    const int E_i = run_eq + e_before + __popc(be & lt_mask);
-    const bool kept = gt || (eq && E_i < need);
-    if (kept) out[out_base + G_i + min(E_i, need)] = idx_base + i;
-    if (!drop_found) {
-      const unsigned dropped = __ballot_sync(0xffffffffu, valid && !kept);
-      if (dropped) {
-        if (lane == 0) atomicMin(&s.first_drop, idx_base + base + warp * 32 + __ffs(dropped) - 1);
-        drop_found = true;  // later tiles only hold larger indices
+    int g_run = run_gt + g_before, e_run = run_eq + e_before;
+#pragma unroll
+    for (int r = 0; r < kEmitR; ++r) {
+      const int i = wbase + r * 32 + lane;
+      const bool valid = i < n;
+      const bool gt = (bg[r] >> lane) & 1u, eq = (be[r] >> lane) & 1u;
+      const int G_i = g_run + __popc(bg[r] & lt_mask);
+      const int E_i = e_run + __popc(be[r] & lt_mask);
+      const bool kept = gt || (eq && E_i < need);
+      if (kept) out[out_base + G_i + min(E_i, need)] = idx_base + i;
+      if (!drop_found) {
+        const unsigned dropped = __ballot_sync(0xffffffffu, valid && !kept);
+        if (dropped) {
+          if (lane == 0) atomicMin(&s.first_drop, idx_base + wbase + r * 32 + __ffs(dropped) - 1);
+          drop_found = true;  // later keys of this warp only hold larger indices
+        }
       }
+      g_run += __popc(bg[r]);
+      e_run += __popc(be[r]);
     }
     run_gt += g_tot;
     run_eq += e_tot;
