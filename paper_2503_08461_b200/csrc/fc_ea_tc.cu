@@ -384,6 +384,10 @@ __global__ void __launch_bounds__(kEaThreads, 1)
         const unsigned char* krow = ring + (p % kStages) * kStageBytes + grp * (kTileM * 128) +
                                     (trow >> 3) * 1024 + (trow & 7) * 128;
         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sl * kSlotCols + grp * 64);
+        // K . mu (column 128) rides along with the first Y load: one wait for both
+        uint32_t lin_r = 0;
+        if (grp == 0)
+          tc::tmem_ld_x1_async(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sl * kSlotCols + 128), lin_r);
 #pragma unroll
         for (int hcol = 0; hcol < 2; ++hcol) {
           tc::tmem_ld_32x32b_x32(taddr + (uint32_t)(hcol * 32), y);
@@ -397,12 +401,8 @@ __global__ void __launch_bounds__(kEaThreads, 1)
             for (int e = 0; e < 8; ++e) acc = fmaf(y[c * 8 + e], kx[e], acc);
           }
         }
-        float lin = 0.f;
-        if (grp == 0) {
-          float l1[16];
-          tc::tmem_ld_32x32b_x16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sl * kSlotCols + 128), l1);
-          lin = l1[0];
-        }
+        tc::reg_after_wait(lin_r);
+        const float lin = __uint_as_float(lin_r);
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);

@@ -184,6 +184,13 @@ __device__ __forceinline__ void tmem_ld_wait16(uint32_t (&r)[16]) {
                : "memory");
 }
 
+// One fp32 column per lane, issued without a wait (consume after a later wait::ld
+// plus reg_after_wait on the same register).
+__device__ __forceinline__ void tmem_ld_x1_async(uint32_t taddr, uint32_t& r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+}
+__device__ __forceinline__ void reg_after_wait(uint32_t& r) { asm volatile("" : "+r"(r)::"memory"); }
+
 __device__ __forceinline__ void tmem_ld_wait16x2(uint32_t (&a)[16], uint32_t (&b)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;"
                : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]),
