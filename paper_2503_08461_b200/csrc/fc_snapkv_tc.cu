@@ -181,25 +181,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
         for (int hf = 0; hf < kHalves; ++hf)
           tc::tma_load_2d(qbuf + qb * plan.q_bytes + hf * kWin * 128, &qmap, &q_full[qb], hf * 64, qrow);
-        const int64_t row_l = (int64_t)l * g.num_blocks * 2 * g.H * g.bs + (int64_t)h * g.bs;
-        for (int k = 0; k < ntiles; ++k, ++gtile) {
-          const int st = gtile % kTcStages;
+      }
+      // K tiles: lane c issues chunk c's boxes (one round of issue per tile)
+      const int64_t row_l = (int64_t)l * g.num_blocks * 2 * g.H * g.bs + (int64_t)h * g.bs;
+      for (int k = 0; k < ntiles; ++k, ++gtile) {
+        const int st = gtile % kTcStages;
+        const int n_chunks = min(chunks, nb - k * chunks);
+        if (lane == 0) {
           tc::mbar_wait(&st_empty[st], ((gtile / kTcStages) & 1) ^ 1);
-          const int n_chunks = min(chunks, nb - k * chunks);
           if (k == 0) FC_STAMP(it, 0);
           if (k == ntiles - 1) FC_STAMP(it, 1);
           tc::mbar_expect_tx(&st_full[st], (uint32_t)(n_chunks * g.bs * D * 2));
-          unsigned char* dst = stages + st * plan.tile_bytes;
-          for (int c = 0; c < n_chunks; ++c) {
-            const int64_t row0 = row_l + (int64_t)ptab[k * chunks + c] * 2 * g.H * g.bs;
-#pragma unroll
-            for (int hf = 0; hf < kHalves; ++hf)
-              tc::tma_load_2d(dst + hf * kTileM * 128 + c * g.bs * 128, &kmap, &st_full[st],
-                              hf * 64, (int)row0);
-          }
         }
-      } else {
-        gtile += ntiles;
+        __syncwarp();
+        unsigned char* dst = stages + st * plan.tile_bytes;
+        for (int c = lane; c < n_chunks; c += 32) {
+          const int64_t row0 = row_l + (int64_t)ptab[k * chunks + c] * 2 * g.H * g.bs;
+#pragma unroll
+          for (int hf = 0; hf < kHalves; ++hf)
+            tc::tma_load_2d(dst + hf * kTileM * 128 + c * g.bs * 128, &kmap, &st_full[st],
+                            hf * 64, (int)row0);
+        }
       }
     }
   } else if (warp == 1) {
