@@ -199,6 +199,16 @@ def traffic_from_profile(config: str):
         return None
 
 
+def _scaled_traffic(config: str, alg_bytes: int):
+    path = os.path.join(ROOT, "profiles", f"ncu_{config}.json")
+    try:
+        with open(path) as f:
+            ratio = json.load(f).get("traffic_over_alg")
+        return None if ratio is None else ratio * alg_bytes
+    except (OSError, ValueError):
+        return None
+
+
 def _allreduce(value: float, op: str, device) -> float:
     """Max/sum over ranks (NCCL on the GPU tensor, gloo on a CPU copy)."""
     import torch
@@ -314,9 +324,12 @@ def run_churn_bench(args, rank, world, local_rank):
                    "pool_capacity_bytes_per_gpu": capacity,
                    "parallelism": f"LPT request shards x{world}; no data-path collective",
                    "timing": "CUDA events around each wave's compress_batch, summed"},
-        "roofline": {"bound": "hbm", "kernel": "press_kernel<EXPECTED_ATTENTION>",
+        "roofline": {"bound": "hbm", "kernel": "ea_tc_kernel (one launch per admission wave)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic_from_profile("c4"),
+                     "frac": achieved / peak, "frac_of_nominal_8tbs": achieved / 8000.0,
+                     "traffic": _scaled_traffic("c4w", abytes),
+                     "traffic_note": "DRAM bytes per step = ncu traffic/algorithmic ratio of one "
+                                     "c4w wave (profiles/ncu_c4w.json) x this step's algorithmic bytes",
                      "alg_bytes_per_step": abytes},
         "churn": {"waves": r0.waves, "wave_sizes": r0.wave_sizes, "peak_bytes": r0.peak_bytes,
                   "max_fragmentation": r0.max_fragmentation,
