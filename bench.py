@@ -50,6 +50,8 @@ CONFIGS = {
     "c2d": "decode after compression: config 2's batch (32 x 1088 tokens, Knorm 50% -> 544) "
            "then 64 decode steps, each = append one token per request + per layer write K/V and "
            "paged attention over the compacted blocks (SURVEY.md §8(f) row 2)",
+    "c2p": "prefill KV ingest (P.Store): config 2's batch (32 x 1088 tokens) written layer by "
+           "layer from the varlen [rows, H, D] prefill layout into the paged blocks",
     "c5": "synthetic serving trace at 40 req/s (2000 requests, highload shape), request-sharded "
           "by NCCL occupancy exchange, mixed Knorm/SnapKV, TTFT and compression throughput",
 }
@@ -446,6 +448,62 @@ def run_decode_bench(args, rank, world, local_rank):
     }
 
 
+def run_prefill_bench(args, rank, world, local_rank):
+    """P.Store: write_prefill_kv of every layer of config 2's batch (HBM read + write)."""
+    import torch
+
+    from paper_2503_08461_b200 import KVCachePool, kv_bytes
+
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    cfg, dtype, specs, _ = workload("c2")
+    n, L, H, D = len(specs), cfg.num_layers, cfg.num_kv_heads, cfg.head_dim
+    rows = sum(s.total_tokens for s in specs)
+    cap = sum(kv_bytes(cfg, s.total_tokens) for s in specs)
+    pool = KVCachePool(cfg, cap, device=device, kv_dtype=dtype, max_handles=2 * n,
+                       max_tokens_per_handle=max(s.total_tokens for s in specs) + 64)
+    tdt = getattr(torch, dtype)
+    gen = torch.Generator(device=device).manual_seed(rank)
+    k = torch.randn((L, rows, H, D), generator=gen, device=device).to(tdt)
+    v = torch.randn((L, rows, H, D), generator=gen, device=device).to(tdt)
+    stream = torch.cuda.current_stream(device)
+    rids = [rank * 1_000_000 + i for i in range(n)]
+    from paper_2503_08461_b200 import _native
+
+    times, launches = [], 0
+    for step in range(args.warmup + args.steps):
+        hs = pool.allocate_batch(rids, specs, 0.0)
+        torch.cuda.synchronize(device)
+        l0 = _native.launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for layer in range(L):
+            pool.write_prefill_kv(hs, layer, k[layer], v[layer])
+        e1.record(stream)
+        e1.synchronize()
+        if step >= args.warmup:
+            times.append(e0.elapsed_time(e1))
+            launches += _native.launch_count() - l0
+        pool.release_batch(hs, 1.0)
+    ms = statistics.mean(times)
+    max_ms = _allreduce(sum(times), "max", device)
+    peak, peak_kind = measured_peak()
+    moved = 2 * cap                                   # read the varlen K/V, write the blocks
+    achieved = moved / (ms / 1e3) / 1e9
+    return {
+        "metric": "prefill KV ingested tokens/s", "value": rows * world * len(times) / (max_ms / 1e3),
+        "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": max_ms / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16", "data": "synthetic (random K/V)",
+        "config": {"workload": f"c2p: {CONFIGS['c2p']}", "requests_per_gpu": n,
+                   "timing": "CUDA events around the 32 per-layer write_prefill_kv calls"},
+        "roofline": {"bound": "hbm", "kernel": "write_prefill_kernel", "achieved": achieved,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "alg_bytes_per_step": moved},
+        "gpu_launches": launches,
+    }
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -681,7 +739,7 @@ def _cpu_model():
 
 
 def run_reference(args):
-    cfg, dtype, specs, comp = workload(args.config if args.config not in ("c5", "c2d") else "c2")
+    cfg, dtype, specs, comp = workload(args.config if args.config not in ("c5", "c2d", "c2p") else "c2")
     times = []
     last = None
     for i in range(args.warmup + args.steps):
@@ -743,10 +801,12 @@ def main():
         result = run_serving_bench(args, rank, world, local_rank)
     elif args.config == "c2d":
         result = run_decode_bench(args, rank, world, local_rank)
+    elif args.config == "c2p":
+        result = run_prefill_bench(args, rank, world, local_rank)
     else:
         result = run_ours(args, rank, world, local_rank)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cfg, dtype, specs, comp = workload(args.config if args.config not in ("c5", "c2d") else "c2")
+        cfg, dtype, specs, comp = workload(args.config if args.config not in ("c5", "c2d", "c2p") else "c2")
         result["cpu_baseline"] = cpu_reference(args, cfg, dtype, specs, comp)
     if rank == 0:
         print(json.dumps(result), flush=True)

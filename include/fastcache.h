@@ -28,6 +28,7 @@
  *   fc_synth_fill           <- (bench input generator; stands in for P.Store(M.Prefill)
  *                              PAPER.md:246)
  *   fc_pool_store_tokens    <- P.Store (prefill KV ingest)
+ *   fc_pool_write_prefill_kv <- P.Store per layer, batched varlen (the prefill's KV writes)
  *
  * Error convention (pool.py:31-47, kv.py:34-43): functions return fc_status;
  * FC_ERR_CAPACITY fills (requested, available) out-params; fc_last_error()
@@ -198,6 +199,16 @@ FC_API fc_status fc_pool_compress_host_batch(fc_pool* pool, int32_t n, const int
 FC_API fc_status fc_pool_append(fc_pool* pool, int32_t n, const int64_t* handle_ids,
                          const int64_t* tokens, uint64_t* requested_out, uint64_t* available_out,
                          void* stream);
+
+/* P.Store: one layer of the prefill's K and V for n handles in
+ * the varlen layout k, v = [cu_seqlens[n]][Hkv][D] (pool dtype, device):
+ * rows cu_seqlens[i] .. cu_seqlens[i+1]-1 (host array, cu_seqlens[0] = 0) go
+ * to tokens tok_begin[i] + j of handle i (tok_begin NULL = 0). Chunked
+ * prefill calls it once per chunk with the chunk's token offsets. */
+FC_API fc_status fc_pool_write_prefill_kv(fc_pool* pool, int32_t layer, int32_t n,
+                                   const int64_t* handle_ids, const int64_t* cu_seqlens,
+                                   const int64_t* tok_begin, const void* k, const void* v,
+                                   void* stream);
 
 /* Decode over the compacted blocks, one layer at a time. fc_pool_write_kv
  * writes one token's K and V per handle (k, v: [n][Hkv][D], pool dtype) at

@@ -43,7 +43,7 @@ EXPORTS = (
     "fc_pool_release_batch", "fc_pool_get_stats", "fc_pool_synchronize", "fc_pool_block_table",
     "fc_pool_store_tokens", "fc_pool_load_tokens", "fc_synth_fill", "fc_compress_tensor",
     "fc_pool_set_profiling", "fc_pool_last_profile", "fc_pool_compress_host_batch",
-    "fc_pool_write_kv", "fc_pool_decode_attention",
+    "fc_pool_write_kv", "fc_pool_decode_attention", "fc_pool_write_prefill_kv",
 )
 
 
@@ -122,6 +122,7 @@ _SIGS = {
                                            _PU64, _PU64, _P]),
     "fc_pool_append": (_I32, [_P, _I32, _PI64, _PI64, _PU64, _PU64, _P]),
     "fc_pool_write_kv": (_I32, [_P, _I32, _I32, _PI64, _PI64, _P, _P, _P]),
+    "fc_pool_write_prefill_kv": (_I32, [_P, _I32, _I32, _PI64, _PI64, _PI64, _P, _P, _P]),
     "fc_pool_decode_attention": (_I32, [_P, _I32, _I32, _PI64, _I32, ctypes.c_float, _P, _P, _P]),
     "fc_pool_release_batch": (_I32, [_P, _I32, _PI64, _P]),
     "fc_pool_get_stats": (_I32, [_P, ctypes.POINTER(PoolStatsC)]),

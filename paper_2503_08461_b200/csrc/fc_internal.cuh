@@ -95,6 +95,17 @@ struct KVWriteBatch {
   KVWriteReq req[kMaxDecode];
 };
 
+// One request of a prefill K/V write (fc_pool_write_prefill_kv).
+struct PrefillReq {
+  int64_t row0;   // first row of this request in the varlen k / v buffers
+  int64_t tok0;   // first handle token written
+  int32_t slot, n;
+};
+struct PrefillBatch {
+  int32_t n, layer;
+  PrefillReq req[kMaxBatch];
+};
+
 struct PressParams {
   int32_t kind, factor, window, pool_kernel, n_sink, num_q_heads;
   // SEEDEDLINEAR: device table [factor][factor]; row m-1 = the reference's
@@ -208,6 +219,9 @@ fc_status launch_synth(const Geom& g, int dtype, char* arena, const int32_t* tab
 fc_status launch_store(const Geom& g, char* arena, const int32_t* table_row, int64_t tok_begin,
                        int64_t n_tok, const void* src, bool to_blocks, cudaStream_t stream,
                        int kv0 = 0, int nkv = 2);
+fc_status launch_write_prefill(const Geom& g, char* arena, const int32_t* table, int layer, int n,
+                               const PrefillReq* reqs, const void* k, const void* v,
+                               cudaStream_t stream);
 fc_status launch_gather_host(const Geom& g, char* arena, const int32_t* table, int n,
                              const HostGatherReq* reqs, const int32_t* kept_idx, int kv,
                              cudaStream_t stream);

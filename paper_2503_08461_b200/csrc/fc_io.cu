@@ -310,4 +310,79 @@ fc_status launch_compress_tensor(const void* src, int64_t n, int64_t d, int dtyp
   return cuda_check(cudaGetLastError(), "compress_tensor_kernel");
 }
 
+
+// ---------------------------------------------------------------------------
+// P.Store: one layer of the prefill's K/V for a batch of
+// requests, varlen layout k, v = [sum_i n_i][H][D] (request i's rows start at
+// cu[i]), written to tokens tok0[i] + j of each handle's blocks. One 16-B
+// vector per thread; reads are fully coalesced, writes land as 256-B rows in
+// the (layer, K|V, head) chunk of their block.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    write_prefill_kernel(char* __restrict__ arena, const int32_t* __restrict__ table, const Geom g,
+                         const __grid_constant__ PrefillBatch b, const char* __restrict__ k,
+                         const char* __restrict__ v) {
+  const PrefillReq rq = b.req[blockIdx.y];
+  const int vpr = (int)(g.row_bytes / 16);
+  // token-major order: the reads stream the varlen rows; each token's 2*H rows of
+  // 256 B land in their (K|V, head) chunks (a chunk-contiguous order that streams
+  // the writes instead measured 11% slower)
+  const int64_t per_tok = (int64_t)2 * g.H * vpr;
+  const int64_t total = (int64_t)rq.n * per_tok;
+  const int32_t* row_tab = table + (int64_t)rq.slot * g.max_bpr;
+  constexpr int kUnroll = 4;  // 4 independent 16-B loads in flight per thread
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t x0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x0 < total; x0 += stride * kUnroll) {
+    uint4 buf[kUnroll];
+    char* dst[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t x = x0 + u * stride;
+      dst[u] = nullptr;
+      if (x < total) {
+        const int64_t j = x / per_tok;
+        const int rem = (int)(x - j * per_tok);
+        const int kv = rem / (g.H * vpr), hv = rem % (g.H * vpr);
+        const int h = hv / vpr, vec = hv % vpr;
+        buf[u] = ld_stream((kv ? v : k) + ((rq.row0 + j) * g.H + h) * g.row_bytes + vec * 16);
+        const int64_t t = rq.tok0 + j;
+        dst[u] = arena + g.seg_base(b.layer, kv, h) + (int64_t)row_tab[t >> g.bs_shift] * g.block_stride +
+                 (t & (g.bs - 1)) * g.row_bytes + vec * 16;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (dst[u]) st_stream(dst[u], buf[u]);
+  }
+}
+
+fc_status launch_write_prefill(const Geom& g, char* arena, const int32_t* table, int layer, int n,
+                               const PrefillReq* reqs, const void* k, const void* v,
+                               cudaStream_t stream) {
+  for (int c = 0; c < n; c += kMaxBatch) {
+    PrefillBatch b;
+    memset(&b, 0, sizeof(b));
+    b.n = n - c < kMaxBatch ? n - c : kMaxBatch;
+    b.layer = layer;
+    int64_t max_vecs = 0;
+    for (int i = 0; i < b.n; ++i) {
+      b.req[i] = reqs[c + i];
+      const int64_t vv = (int64_t)b.req[i].n * 2 * g.H * (g.row_bytes / 16);
+      max_vecs = vv > max_vecs ? vv : max_vecs;
+    }
+    if (max_vecs == 0) continue;
+    int64_t gx = (max_vecs + 4095) / 4096;
+    const int64_t cap = (148LL * 8 + b.n - 1) / b.n;
+    if (gx > cap) gx = cap;
+    if (gx < 1) gx = 1;
+    write_prefill_kernel<<<dim3((unsigned)gx, (unsigned)b.n), 256, 0, stream>>>(arena, table, g, b,
+                                                                               (const char*)k,
+                                                                               (const char*)v);
+    note_launch();
+    fc_status st = cuda_check(cudaGetLastError(), "write_prefill_kernel");
+    if (st != FC_OK) return st;
+  }
+  return FC_OK;
+}
+
 }  // namespace fc

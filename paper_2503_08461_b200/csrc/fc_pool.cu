@@ -898,6 +898,35 @@ fc_status fc_pool_write_kv(fc_pool* p, int32_t layer, int32_t n, const int64_t* 
   return FC_OK;
 }
 
+fc_status fc_pool_write_prefill_kv(fc_pool* p, int32_t layer, int32_t n, const int64_t* handle_ids,
+                                   const int64_t* cu_seqlens, const int64_t* tok_begin,
+                                   const void* k, const void* v, void* stream) {
+  if (!p || n < 0 || (n > 0 && (!handle_ids || !cu_seqlens || !k || !v)))
+    return set_error(FC_ERR_INVALID_ARG, "bad arguments");
+  if (layer < 0 || layer >= p->g.L) return set_error(FC_ERR_INVALID_ARG, "layer out of range");
+  if (((uintptr_t)k) % 16 || ((uintptr_t)v) % 16)
+    return set_error(FC_ERR_INVALID_ARG, "k / v must be 16-byte aligned");
+  if (n > 0 && cu_seqlens[0] != 0) return set_error(FC_ERR_INVALID_ARG, "cu_seqlens[0] must be 0");
+  std::vector<PrefillReq> reqs(n);
+  for (int i = 0; i < n; ++i) {
+    int32_t s;
+    fc_status st = lookup(p, handle_ids[i], &s);
+    if (st != FC_OK) return st;
+    for (int j = 0; j < i; ++j)
+      if (reqs[j].slot == s) return set_error(FC_ERR_INVALID_ARG, "handle repeated in batch");
+    const int64_t cnt = cu_seqlens[i + 1] - cu_seqlens[i];
+    const int64_t t0 = tok_begin ? tok_begin[i] : 0;
+    if (cnt < 0 || t0 < 0 || t0 + cnt > p->slots[s].tokens)
+      return set_error(FC_ERR_INVALID_ARG, "rows of request %d fall outside its %lld tokens", i,
+                       (long long)p->slots[s].tokens);
+    reqs[i] = PrefillReq{cu_seqlens[i], t0, s, (int32_t)cnt};
+  }
+  if (n == 0) return FC_OK;
+  DeviceGuard guard(p->device);
+  return launch_write_prefill(p->g, p->arena, p->d_table, layer, n, reqs.data(), k, v,
+                              (cudaStream_t)stream);
+}
+
 fc_status fc_pool_decode_attention(fc_pool* p, int32_t layer, int32_t n, const int64_t* handle_ids,
                                    int32_t num_q_heads, float scale, const void* q, void* out,
                                    void* stream) {

@@ -305,6 +305,12 @@ class _NativePool:
                                               ctypes.c_void_p(k.data_ptr()),
                                               ctypes.c_void_p(v.data_ptr()), self.stream()))
 
+    def write_prefill(self, layer: int, handle_ids, cu_seqlens, tok_begin, k, v) -> None:
+        tb = nat.i64_array(tok_begin) if tok_begin is not None else None
+        self._check(self.lib.fc_pool_write_prefill_kv(
+            self.ptr, layer, len(handle_ids), nat.i64_array(handle_ids), nat.i64_array(cu_seqlens),
+            tb, ctypes.c_void_p(k.data_ptr()), ctypes.c_void_p(v.data_ptr()), self.stream()))
+
     def decode_attention(self, layer: int, handle_ids, num_q_heads: int, scale: float, q,
                          out) -> None:
         self._check(self.lib.fc_pool_decode_attention(
@@ -673,6 +679,31 @@ class KVCachePool:
             h.bytes += needed
             self._apply(now, "append", h.handle_id, needed)
         return handles
+
+    def write_prefill_kv(self, handles: Sequence[CacheHandle], layer: int, k, v,
+                         seq_lens: Sequence[int] | None = None,
+                         tok_begin: Sequence[int] | None = None) -> None:
+        """P.Store: one layer of the prefill's K and V for a batch, varlen
+        layout ``k``, ``v`` = [sum_i n_i, Hkv, D] (pool dtype, CUDA) with request i's rows
+        after request i-1's; ``seq_lens[i]`` rows (default: the handle's tokens) land at
+        tokens ``tok_begin[i]`` + j (default 0) -- chunked prefill passes the chunk."""
+        nv = self._need_native()
+        cfg = self.config
+        handles = list(handles)
+        lens = [h.spec.total_tokens for h in handles] if seq_lens is None else [int(x) for x in seq_lens]
+        if len(lens) != len(handles):
+            raise ValueError("seq_lens needs one entry per handle")
+        rows = sum(lens)
+        want = (rows, cfg.num_kv_heads, cfg.head_dim)
+        for t in (k, v):
+            if tuple(t.shape) != want or t.dtype != nv.torch_dtype or t.device != nv.device \
+                    or not t.is_contiguous():
+                raise ValueError(f"k and v must be contiguous {nv.kv_dtype} CUDA tensors {want}")
+        cu = [0]
+        for n in lens:
+            cu.append(cu[-1] + n)
+        if handles:
+            nv.write_prefill(layer, [h.handle_id for h in handles], cu, tok_begin, k, v)
 
     def write_decode_kv(self, handles: Sequence[CacheHandle], layer: int, k, v,
                         positions: Sequence[int] | None = None) -> None:

@@ -142,6 +142,13 @@ def serve(pool: KVCachePool, requests: list[Request], *, max_prefill: int = 8,
     gen = torch.Generator(device=dev).manual_seed(seed)
     q_all = torch.randn((max_compress, cfg.num_layers, hq, 32, cfg.head_dim), generator=gen,
                         device=dev, dtype=torch.float32).to(pool._native.torch_dtype)
+    # synthetic prefill output (varlen [rows, Hkv, D] per layer, the layout attention
+    # produces); written into the blocks with the real P.Store path, layer by layer
+    max_rows = max_prefill * max(r.tokens for r in requests) if requests else 0
+    pf_k = torch.randn((max_rows, cfg.num_kv_heads, cfg.head_dim), generator=gen, device=dev,
+                       dtype=torch.float32).to(pool._native.torch_dtype)
+    pf_v = torch.randn((max_rows, cfg.num_kv_heads, cfg.head_dim), generator=gen, device=dev,
+                       dtype=torch.float32).to(pool._native.torch_dtype)
     events: list = []
     seq = 0
 
@@ -208,7 +215,9 @@ def serve(pool: KVCachePool, requests: list[Request], *, max_prefill: int = 8,
             busy["prefill"] = False
             hs = pool.allocate_batch([r.rid for r in payload],
                                      [split_modalities(r.image, r.text) for r in payload], now)
-            pool.synth_fill(hs, seed=seed)            # stands in for the prefill's KV writes
+            rows = sum(r.tokens for r in payload)
+            for layer in range(cfg.num_layers):       # the prefill's KV writes (P.Store)
+                pool.write_prefill_kv(hs, layer, pf_k[:rows], pf_v[:rows])
             for r, h in zip(payload, hs):
                 handles[r.rid] = h
                 r.prefill_end = now
