@@ -348,7 +348,13 @@ __device__ void score_ea(const char* __restrict__ seg, const Geom& g, const int3
 #ifndef FC_KNORM_ASYNC  // Knorm compaction through a cp.async SMEM ring (fc_select.cuh)
 #define FC_KNORM_ASYNC 1
 #endif
-constexpr int kKnRanks = 16, kKnBufs = 4;
+#ifndef FC_KN_RANKS
+#define FC_KN_RANKS 16
+#endif
+#ifndef FC_KN_BUFS
+#define FC_KN_BUFS 4
+#endif
+constexpr int kKnRanks = FC_KN_RANKS, kKnBufs = FC_KN_BUFS;
 
 struct SmemPlan {
   int nb;          // table entries per table
