@@ -36,7 +36,10 @@ struct DecodeCfg {
   static constexpr int kVpr = D / kEPV;
   static_assert(kVpr >= 1 && kVpr <= 32 && (32 % kVpr) == 0, "row must split evenly over a warp");
   static constexpr int kRows = 32 / kVpr;
-  static constexpr int kTile = G >= 4 ? 4 : 8;  // rows in flight vs registers for G heads
+#ifndef FC_DEC_TILE1
+#define FC_DEC_TILE1 4
+#endif
+  static constexpr int kTile = G >= 4 ? 4 : (G == 1 ? FC_DEC_TILE1 : 8);  // rows in flight vs registers
 };
 
 __device__ __forceinline__ void merge_state(float& m, float& l, float* acc, float m_o, float l_o,
@@ -49,8 +52,11 @@ __device__ __forceinline__ void merge_state(float& m, float& l, float* acc, floa
   m = mn;
 }
 
+#ifndef FC_DEC_MINB1
+#define FC_DEC_MINB1 6
+#endif
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(kDecodeThreads)
+__global__ void __launch_bounds__(kDecodeThreads, G == 1 ? FC_DEC_MINB1 : 1)
     decode_attn_kernel(const char* __restrict__ arena, const int32_t* __restrict__ table,
                        const Geom g, const __grid_constant__ DecodeBatch b,
                        const T* __restrict__ q, T* __restrict__ out, float scale_log2,
