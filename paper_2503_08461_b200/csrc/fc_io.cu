@@ -330,7 +330,10 @@ __global__ void __launch_bounds__(256)
   const int64_t per_tok = (int64_t)2 * g.H * vpr;
   const int64_t total = (int64_t)rq.n * per_tok;
   const int32_t* row_tab = table + (int64_t)rq.slot * g.max_bpr;
-  constexpr int kUnroll = 4;  // 4 independent 16-B loads in flight per thread
+#ifndef FC_PF_UNROLL
+#define FC_PF_UNROLL 2
+#endif
+  constexpr int kUnroll = FC_PF_UNROLL;  // independent 16-B loads in flight per thread
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t x0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x0 < total; x0 += stride * kUnroll) {
     uint4 buf[kUnroll];
@@ -371,8 +374,11 @@ fc_status launch_write_prefill(const Geom& g, char* arena, const int32_t* table,
       max_vecs = vv > max_vecs ? vv : max_vecs;
     }
     if (max_vecs == 0) continue;
+#ifndef FC_PF_CTAS
+#define FC_PF_CTAS 64
+#endif
     int64_t gx = (max_vecs + 4095) / 4096;
-    const int64_t cap = (148LL * 8 + b.n - 1) / b.n;
+    const int64_t cap = (148LL * FC_PF_CTAS + b.n - 1) / b.n;
     if (gx > cap) gx = cap;
     if (gx < 1) gx = 1;
     write_prefill_kernel<<<dim3((unsigned)gx, (unsigned)b.n), 256, 0, stream>>>(arena, table, g, b,
