@@ -417,8 +417,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (ct == 0) FC_STAMP(it, 12);
       // hand the kept list to the compactors (double-buffered)
       tc::mbar_wait(&job_empty[jb], ((it >> 1) & 1) ^ 1);
+      if (ct == 0) FC_STAMP(it, 13);
       int32_t* idx = idxbuf + jb * t_stride;
       for (int i = ct; i < nb; i += kThreads) ctab[jb * nb_stride + i] = table[(int64_t)q.slot * g.max_bpr + i];
+      if (ct == 0) FC_STAMP(it, 14);
       if (b.per_segment && q.seg0 < T_len) {
         select_emit<Consumers>(keys, q.seg0, q.K0, idx, 0, 0, ss);
         select_emit<Consumers>(keys + q.seg0, T_len - q.seg0, K - q.K0, idx, q.K0, q.seg0, ss);

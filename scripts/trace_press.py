@@ -54,3 +54,7 @@ if len(sys.argv) > 2 and sys.argv[2] == "fine":
     print("fine: p3->pool %.2f  pool->keys %.2f  keys->ctab %.2f  ctab->handoff %.2f us" % (
         (d[:, :, 0] - d[:, :, 4]).mean(), (d[:, :, 1] - d[:, :, 0]).mean(),
         (d[:, :, 2] - d[:, :, 1]).mean(), (d[:, :, 5] - d[:, :, 2]).mean()))
+if len(sys.argv) > 2 and sys.argv[2] == "sub":
+    print("select: keys->job_empty %.2f  ctab copy %.2f  select+emit+handoff %.2f us" % (
+        (d[:, :, 13] - d[:, :, 12]).mean(), (d[:, :, 14] - d[:, :, 13]).mean(),
+        (d[:, :, 5] - d[:, :, 14]).mean()))
