@@ -97,3 +97,37 @@ def test_device_pool_without_gpu_raises():
 
     with pytest.raises(nat.NativeUnavailable):
         KVCachePool(ModelConfig("tiny", 4, 8, 64, 4), 1 << 30, device="cuda:0")
+
+
+def test_device_only_calls_on_a_ledger_pool_fail_loudly():
+    """The payload calls (host-resident compress, P.Store, decode) have no CPU fallback:
+    on a ledger-only pool they raise instead of silently doing nothing."""
+    import torch
+
+    from paper_2503_08461_b200 import (
+        CompressorSpec,
+        KVCachePool,
+        ModelConfig,
+        PressKind,
+        split_modalities,
+    )
+
+    cfg = ModelConfig("tiny", 2, 2, 64, 2)
+    pool = KVCachePool(cfg, 1 << 30)
+    h = pool.allocate(0, split_modalities(0, 8), 0.0)
+    host = torch.zeros((2, 2, 2, 8, 64), dtype=torch.float16)
+    with pytest.raises(nat.NativeUnavailable):
+        pool.compress_batch([h], CompressorSpec(factor=2, press=PressKind.KNORM), 1.0,
+                            host_kv=[host])
+    assert h.spec.total_tokens == 8          # nothing was transitioned
+    kv = torch.zeros((8, 2, 64), dtype=torch.float16)
+    with pytest.raises(nat.NativeUnavailable):
+        pool.write_prefill_kv([h], 0, kv, kv)
+    with pytest.raises(nat.NativeUnavailable):
+        pool.decode_attention([h], 0, torch.zeros((1, 2, 64), dtype=torch.float16))
+    with pytest.raises(nat.NativeUnavailable):
+        pool.write_decode_kv([h], 0, kv[:1], kv[:1])
+    pool.compress_batch([h], CompressorSpec(factor=2, press=PressKind.KNORM), 1.0)
+    pool.append_decode_batch([h], 1, 2.0)   # the ledger part works without a device
+    assert h.spec.total_tokens == 5
+    pool.verify_conservation()
