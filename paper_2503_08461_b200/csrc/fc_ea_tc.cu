@@ -56,6 +56,9 @@ constexpr int kD = 128;
 constexpr int kStages = 3;
 constexpr int kTileM = 128;
 constexpr int kBRows = 144;                     // 128 Sigma^T rows + mu + 15 zero rows
+#ifndef FC_EA_CITEMS  // compactor 16-B loads in flight per thread per chunk
+#define FC_EA_CITEMS 8
+#endif
 #ifndef FC_EA_CPF  // compactor L2 prefetch distance in chunks (0 measured best: 41.2 vs 42.4 ms at 2)
 #define FC_EA_CPF 0
 #endif
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(kEaThreads, 1)
       if (Compactors::tid() == 0) EA_STAMP(it, 6);
       const Job job = s_job[jb];
       char* seg = arena + g.seg_base(job.l, 0, job.h);
-      compact_rows<kD * 2, Compactors, 8, FC_EA_CPF>(seg, g, ctab + jb * nb_stride, ctab + jb * nb_stride,
+      compact_rows<kD * 2, Compactors, FC_EA_CITEMS, FC_EA_CPF>(seg, g, ctab + jb * nb_stride, ctab + jb * nb_stride,
                                           idxbuf + jb * k_stride, job.K, job.first_moved);
       Compactors::sync();
       if (Compactors::tid() == 0) {
