@@ -47,9 +47,13 @@ __device__ __forceinline__ void score_knorm(const char* __restrict__ seg, const 
   constexpr bool kExactSquare = sizeof(T) == 2;
   const int lr = threadIdx.x % kLPR, rp = threadIdx.x / kLPR;
   // bulk L2 prefetch of whole block chunks (bs rows each) kPfIters iterations ahead
-  constexpr int kPfIters = 2;
+#ifndef FC_KN_SPF
+#define FC_KN_SPF 2
+#endif
+  constexpr int kPfIters = FC_KN_SPF;
   const int chunk_bytes = g.bs * kRowBytes;
   auto prefetch_rows = [&](int r0, int r1) {
+    if (kPfIters == 0) return;
     for (int c = (r0 >> g.bs_shift) + threadIdx.x; c < ((min(r1, T_len) + g.bs - 1) >> g.bs_shift);
          c += kThreads)
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
