@@ -686,10 +686,9 @@ def cpu_reference(args, cfg, dtype, specs, comp, reps: int | None = None):
     np_dt = {"float16": np.float16, "float32": np.float32, "bfloat16": np.float32}[dtype]
     kv = rng.standard_normal((cfg.num_layers, 2, cfg.num_kv_heads, s0.total_tokens, cfg.head_dim),
                              dtype=np.float32).astype(np_dt)
-    if comp.press is not PressKind.KNORM:
-        note = " (Knorm port used as the CPU reference pass; the SnapKV/EA ports are slower)"
-    else:
-        note = ""
+    if comp.press in (PressKind.SNAPKV, PressKind.EXPECTED_ATTENTION):
+        return cpu_press_sample(cfg, dtype, specs, comp, workers)
+    note = ""
     n_req = reps or workers
     r = cpu_pipeline.time_knorm_requests(kv, segs, comp.factor, n_req, workers,
                                          cfg.bytes_per_element)
@@ -701,6 +700,45 @@ def cpu_reference(args, cfg, dtype, specs, comp, reps: int | None = None):
             "sample": sample, "seconds": r["seconds"],
             "cpu_model": _cpu_model(),
             "literal_reference_path": literal_reference_path(cfg, kv, segs, comp)}
+
+
+def cpu_press_sample(cfg, dtype, specs, comp, workers):
+    """SnapKV / EA on the host: the oracle press (float64 scores, stable top-k, K/V gather)
+    on a bounded sample of (layer, head) pairs of the batch's longest request, extrapolated
+    to every (request, layer, head) of the batch."""
+    import numpy as np
+
+    from oracle import cpu_pipeline
+    from paper_2503_08461_b200 import PressKind
+
+    s0 = max(specs, key=lambda s: s.total_tokens)
+    segs = [seg.token_count for seg in s0.segments]
+    t_len, d = s0.total_tokens, cfg.head_dim
+    rng = np.random.default_rng(0)
+    np_dt = np.float16 if dtype == "float16" else np.float32
+    k = rng.standard_normal((t_len, d), dtype=np.float32).astype(np_dt)
+    v = rng.standard_normal((t_len, d), dtype=np.float32).astype(np_dt)
+    if comp.press is PressKind.SNAPKV:
+        kw = {"q_win": rng.standard_normal((1, comp.window, d)).astype(np.float32),
+              "window": comp.window, "pool_kernel": comp.pool_kernel}
+        kind = "snapkv"
+    else:
+        a = rng.standard_normal((1, d, d))
+        kw = {"mean_q": rng.standard_normal((1, d)) / d ** 0.5, "cov_q": a @ a.transpose(0, 2, 1) / d,
+              "n_sink": comp.n_sink}
+        kind = "expected_attention"
+    n_pairs = 4 * workers
+    r = cpu_pipeline.time_press_pairs(k, v, segs, comp.factor, kind, n_pairs, workers, **kw)
+    # every pair of the batch, scaled by length (the work is linear in T at fixed D)
+    pairs_total = sum(s.total_tokens for s in specs) / t_len * cfg.num_layers * cfg.num_kv_heads
+    secs = r["seconds_per_pair"] * pairs_total / r["workers"]
+    tokens = sum(s.total_tokens for s in specs)
+    return {"value": tokens / secs, "unit": "tokens/s", "cores": r["workers"], "kind": "port",
+            "sample": f"{n_pairs} (layer, head) pairs of a {t_len}-token request "
+                      f"(oracle/cpu_pipeline.press_compress_pair: {kind} float64 scores, stable "
+                      f"top-K_r, K/V gather) on {r['workers']} processes, extrapolated linearly "
+                      f"in tokens to the whole batch", "seconds": secs,
+            "cpu_model": _cpu_model()}
 
 
 def literal_reference_path(cfg, kv, segs, comp, layers: int = 2):

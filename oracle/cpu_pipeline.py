@@ -80,3 +80,48 @@ def time_knorm_requests(kv: np.ndarray, seg_tokens, factor: int, n_requests: int
     tokens = n_requests * kv.shape[3]
     return {"seconds": max(times), "wall_s": wall, "workers": workers, "tokens": tokens,
             "tokens_per_s": tokens / max(times)}
+
+
+# ---------------------------------------------------------------------------
+# SnapKV / ExpectedAttention: the press itself on a sample of (layer, head) pairs
+# ---------------------------------------------------------------------------
+
+
+def press_compress_pair(k_rows, v_rows, seg_tokens, factor: int, press_kind: str, *,
+                        q_win=None, mean_q=None, cov_q=None, window: int = 32,
+                        pool_kernel: int = 7, n_sink: int = 4):
+    """One (request, layer, kv-head): oracle scores (float64), stable top-K_r, K/V gather."""
+    kf = k_rows.astype(np.float32)
+    if press_kind == "snapkv":
+        s = press.snapkv_scores(kf, q_win, window, pool_kernel)
+    else:
+        s = press.expected_attention_scores(kf, v_rows.astype(np.float32), mean_q, cov_q, n_sink)
+    kept = press.select(s, seg_tokens, factor)
+    return kept, k_rows[kept], v_rows[kept]
+
+
+def _pair_worker(reps):
+    args, kw = _SHARED["pair"]
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        press_compress_pair(*args, **kw)
+    return time.perf_counter() - t0
+
+
+def time_press_pairs(k_rows, v_rows, seg_tokens, factor: int, press_kind: str, n_pairs: int,
+                     workers: int | None = None, **kw) -> dict:
+    """Time ``n_pairs`` (layer, head) compressions of one request shape on ``workers``
+    processes; returns seconds per pair (slowest worker x workers / pairs)."""
+    import multiprocessing as mp
+
+    workers = workers or len(os.sched_getaffinity(0))
+    workers = max(1, min(workers, n_pairs))
+    reps = [n_pairs // workers + (1 if i < n_pairs % workers else 0) for i in range(workers)]
+    _SHARED["pair"] = ((k_rows, v_rows, list(seg_tokens), factor, press_kind), kw)
+    if workers == 1:
+        times = [_pair_worker(reps[0])]
+    else:
+        with mp.get_context("fork").Pool(workers) as pool:
+            times = pool.map(_pair_worker, reps)
+    return {"seconds": max(times), "workers": workers, "pairs": n_pairs,
+            "seconds_per_pair": max(times) / max(reps)}
