@@ -110,3 +110,24 @@ def test_decode_explicit_positions_scale_and_errors(cuda):
         pool.decode_attention(hs, 2, q)                       # layer out of range
     with pytest.raises(ValueError):
         pool.decode_attention(hs, 0, q[:, :1].contiguous())   # wrong head count
+
+
+def test_decode_more_requests_than_one_launch(cuda):
+    """300 handles > kMaxDecode (256): the batch is split across launches."""
+    cfg = ModelConfig("m", 1, 2, 64, 2)
+    pool = KVCachePool(cfg, (1 << 16) * cfg.bytes_per_token, device=cuda, kv_dtype="float16",
+                       max_handles=512, max_tokens_per_handle=256, num_q_heads=2)
+    rng = torch.Generator().manual_seed(0)
+    lens = torch.randint(1, 120, (300,), generator=rng).tolist()
+    hs = pool.allocate_batch(list(range(300)), [split_modalities(0, t) for t in lens], 0.0)
+    pool.synth_fill(hs, seed=3)
+    pool.compress_batch(hs, CompressorSpec(factor=2, press=PressKind.KNORM), 1.0)
+    pool.append_decode_batch(hs, 1, 2.0)
+    kv = torch.randn((300, 2, 64), device=cuda).half()
+    pool.write_decode_kv(hs, 0, kv, kv)
+    q = torch.randn((300, 2, 64), device=cuda).half()
+    out = pool.decode_attention(hs, 0, q)
+    for i in (0, 1, 255, 256, 299):
+        cache = pool.load_tokens(hs[i])
+        _check(out[i], _reference(cache[0:1], q[i], 64 ** -0.5)[0], "float16")
+    pool.verify_conservation()

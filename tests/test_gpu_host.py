@@ -158,3 +158,24 @@ def test_host_compress_rejects_pageable_and_bad_shapes(cuda):
     pool.compress_batch([h], comp, 1.0, host_kv=[pinned])
     assert h.spec.total_tokens == 32
     pool.verify_conservation()
+
+
+def test_host_compress_more_requests_than_one_launch(cuda):
+    """150 requests > kMaxBatch (128): press and host-gather launches are chunked."""
+    cfg = ModelConfig("m", 1, 2, 64, 2)
+    rs = [split_modalities(0, 20 + (i * 7) % 90) for i in range(150)]
+    host = _host_kv(cfg, "float16", rs, seed=5)
+    comp = CompressorSpec(factor=3, press=PressKind.KNORM)
+    dev_pool = KVCachePool(cfg, (1 << 16) * cfg.bytes_per_token, device=cuda, kv_dtype="float16",
+                           max_handles=256, max_tokens_per_handle=256)
+    dh = dev_pool.allocate_batch(list(range(150)), rs, 0.0)
+    for h, t in zip(dh, host):
+        dev_pool.store_tokens(h, t.to(cuda))
+    dev_pool.compress_batch(dh, comp, 1.0)
+    host_pool = KVCachePool(cfg, (1 << 16) * cfg.bytes_per_token, device=cuda, kv_dtype="float16",
+                            max_handles=256, max_tokens_per_handle=256)
+    hh = host_pool.allocate_batch(list(range(150)), rs, 0.0)
+    host_pool.compress_batch(hh, comp, 1.0, host_kv=host)
+    for a, b in zip(dh, hh):
+        assert np.array_equal(_bits(dev_pool.load_tokens(a)), _bits(host_pool.load_tokens(b)))
+    host_pool.verify_conservation()
