@@ -132,6 +132,9 @@ __device__ __forceinline__ int b_off(int n, int k) {
 
 using namespace ea;
 
+// T = __half or __nv_bfloat16: the K/V tiles' type; Sigma / mu are split into
+// hi + lo parts of the same type (fp16: ~22 significant bits, bf16: ~16).
+template <typename T>
 __global__ void __launch_bounds__(kEaThreads, 1)
     ea_tc_kernel(char* __restrict__ arena, const int32_t* __restrict__ table, const Geom g,
                  const __grid_constant__ PressBatch b, const PressParams pp,
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(kEaThreads, 1)
   } else if (warp == 1) {
     // ================= MMA issuer =================
     if (lane == 0) {
-      const uint32_t idesc = tc::idesc_f16(0, kTileM, kBRows);
+      const uint32_t idesc = tc::idesc_f16(Elem<T>::kDtype == FC_BF16 ? 1 : 0, kTileM, kBRows);
       const uint32_t bh = tc::smem_u32(bmat), bl = bh + kBBytes;
       int pos = 2, gt = 0;
       for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
@@ -339,12 +342,12 @@ __global__ void __launch_bounds__(kEaThreads, 1)
         for (int i = ct; i < 128 * 8; i += kThreads) {
           const int n = i & 127, c8 = i >> 7;           // 8 chunks of 8 k's
           const int k0 = part * 64 + c8 * 8;
-          __half hi[8], lo[8];
+          T hi[8], lo[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const float x = sig[(c8 * 8 + e) * kD + n];
-            hi[e] = __float2half_rn(x);
-            lo[e] = __float2half_rn(x - __half2float(hi[e]));
+            hi[e] = Elem<T>::from_f(x);
+            lo[e] = Elem<T>::from_f(x - Elem<T>::to_f(hi[e]));
           }
           *reinterpret_cast<uint4*>(bmat + b_off(n, k0)) = *reinterpret_cast<uint4*>(hi);
           *reinterpret_cast<uint4*>(bmat + kBBytes + b_off(n, k0)) = *reinterpret_cast<uint4*>(lo);
@@ -353,9 +356,9 @@ __global__ void __launch_bounds__(kEaThreads, 1)
       }
       for (int k = ct; k < kD; k += kThreads) {
         const float x = mu[k];
-        const __half hi = __float2half_rn(x);
-        *reinterpret_cast<__half*>(bmat + b_off(128, k)) = hi;
-        *reinterpret_cast<__half*>(bmat + kBBytes + b_off(128, k)) = __float2half_rn(x - __half2float(hi));
+        const T hi = Elem<T>::from_f(x);
+        *reinterpret_cast<T*>(bmat + b_off(128, k)) = hi;
+        *reinterpret_cast<T*>(bmat + kBBytes + b_off(128, k)) = Elem<T>::from_f(x - Elem<T>::to_f(hi));
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       Consumers::sync();
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(kEaThreads, 1)
             const int chunk = hcol * 4 + c;
             const uint4 raw = *reinterpret_cast<const uint4*>(krow + ((chunk ^ (trow & 7)) << 4));
             float kx[8];
-            unpack16<__half>(raw, kx);
+            unpack16<T>(raw, kx);
 #pragma unroll
             for (int e = 0; e < 8; ++e) acc = fmaf(y[c * 8 + e], kx[e], acc);
           }
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(kEaThreads, 1)
           float vx[8];
           // physical chunk c ^ (row & 7): the 128-B swizzle spreads the 16 rows of a warp
           // over all 32 banks (unswizzled offsets put every lane on the same 4 banks)
-          unpack16<__half>(*reinterpret_cast<const uint4*>(vrow + ((c ^ (row & 7)) << 4)), vx);
+          unpack16<T>(*reinterpret_cast<const uint4*>(vrow + ((c ^ (row & 7)) << 4)), vx);
 #pragma unroll
           for (int e = 0; e < 8; ++e) sq = fmaf(vx[e], vx[e], sq);
         }
@@ -512,7 +515,7 @@ bool ea_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T,
     return e && e[0] == '1';
   }();
   if (forced_simt) return false;
-  if (dtype != FC_F16 || g.D != kD) return false;
+  if ((dtype != FC_F16 && dtype != FC_BF16) || g.D != kD) return false;
   if (pp.num_q_heads != g.H) return false;   // one query head per kv head
   if (g.bs < 8 || g.bs > 128) return false;
   return plan(g.bs, max_T, max_K).total <= 227 * 1024;
@@ -520,12 +523,12 @@ bool ea_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T,
 
 fc_status encode_rows(CUtensorMap* map, const void* base, int dtype, int D, uint64_t rows, int box_rows);
 
-fc_status launch_ea_tc(const Geom& g, char* arena, const int32_t* table, const PressBatch& b,
-                       const PressParams& pp, const fc_press_inputs& in, const fc_press_outputs& out,
-                       int max_K, cudaStream_t stream) {
+fc_status launch_ea_tc(const Geom& g, int dtype, char* arena, const int32_t* table,
+                       const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
+                       const fc_press_outputs& out, int max_K, cudaStream_t stream) {
   CUtensorMap kmap, cmap;
   const uint64_t rows = (uint64_t)g.L * g.num_blocks * 2 * g.H * g.bs;
-  fc_status st = encode_rows(&kmap, arena, FC_F16, g.D, rows, g.bs);
+  fc_status st = encode_rows(&kmap, arena, dtype, g.D, rows, g.bs);
   if (st != FC_OK) return st;
   st = encode_rows(&cmap, in.cov_q, FC_F32, g.D, (uint64_t)b.n_total * g.L * pp.num_q_heads * g.D, 64);
   if (st != FC_OK) return st;
@@ -535,12 +538,15 @@ fc_status launch_ea_tc(const Geom& g, char* arena, const int32_t* table, const P
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = n_items < sms ? n_items : sms;
-  cudaError_t e = cudaFuncSetAttribute(ea_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P.total);
-  if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(ea_tc)");
-  ea_tc_kernel<<<grid, kEaThreads, P.total, stream>>>(arena, table, g, b, pp, kmap, cmap, in.mean_q,
-                                                     out, n_items, max_K);
-  note_launch();
-  return cuda_check(cudaGetLastError(), "ea_tc_kernel");
+  auto launch = [&](auto kern) -> fc_status {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P.total);
+    if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(ea_tc)");
+    kern<<<grid, kEaThreads, P.total, stream>>>(arena, table, g, b, pp, kmap, cmap, in.mean_q, out,
+                                                n_items, max_K);
+    note_launch();
+    return cuda_check(cudaGetLastError(), "ea_tc_kernel");
+  };
+  return dtype == FC_BF16 ? launch(ea_tc_kernel<__nv_bfloat16>) : launch(ea_tc_kernel<__half>);
 }
 
 }  // namespace fc

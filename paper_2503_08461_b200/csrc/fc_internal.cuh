@@ -199,9 +199,9 @@ fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t*
                            const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
                            const fc_press_outputs& out, cudaStream_t stream);
 bool ea_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T, int max_K);
-fc_status launch_ea_tc(const Geom& g, char* arena, const int32_t* table, const PressBatch& b,
-                       const PressParams& pp, const fc_press_inputs& in, const fc_press_outputs& out,
-                       int max_K, cudaStream_t stream);
+fc_status launch_ea_tc(const Geom& g, int dtype, char* arena, const int32_t* table,
+                       const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
+                       const fc_press_outputs& out, int max_K, cudaStream_t stream);
 int64_t press_workspace_floats(const Geom& g, int kind, int window, int num_q_heads, int max_T);
 
 // decode kernels (fc_decode.cu)

@@ -597,7 +597,7 @@ static fc_status launch_one(const Geom& g, char* arena, const int32_t* src, int3
     int max_K = 1;
     for (int i = 0; i < b.n; ++i) max_K = max_K > b.req[i].K ? max_K : b.req[i].K;
     if (ea_tc_supported(g, Elem<T>::kDtype, pp, b.max_T, max_K))
-      return launch_ea_tc(g, arena, src, b, pp, in, out, max_K, stream);
+      return launch_ea_tc(g, Elem<T>::kDtype, arena, src, b, pp, in, out, max_K, stream);
   }
   const SmemPlan plan = smem_plan(KIND, b.max_T, g.bs, D, pp.window, b.in_place != 0, D * (int)sizeof(T));
   const int smem = plan.total();

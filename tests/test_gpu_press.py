@@ -251,6 +251,7 @@ def test_snapkv_parity(cuda, dtype, L, H, gq, D, specs, w, p):
 @pytest.mark.parametrize("dtype,L,H,gq,D,specs,ns", [
     ("float16", 2, 2, 1, 128, [(576, 200), (0, 1024)], 4),               # tcgen05 path
     ("float16", 1, 2, 1, 128, [(576, 7616), (1, 1500), (0, 5), (130, 0)], 4),   # tcgen05, T=8192
+    ("bfloat16", 2, 2, 1, 128, [(576, 200), (0, 1024), (576, 3000)], 4),     # tcgen05, bf16 hi/lo
     ("bfloat16", 1, 2, 2, 64, [(0, 300)], 4),
     ("float32", 1, 1, 2, 128, [(30, 40)], 2),
 ])
