@@ -27,6 +27,9 @@ struct NamedGroup {
 };
 
 constexpr int kRadixBins = 256;  // 8-bit digits, 4 passes
+#ifndef FC_SEL_EXACT
+#define FC_SEL_EXACT 1
+#endif
 
 struct SelectScratch {
   uint32_t hist[2][kRadixBins];   // double-buffered: pass p counts into hist[p & 1]
@@ -34,6 +37,7 @@ struct SelectScratch {
   uint32_t emit_tot[2][kWarps];   // double-buffered packed (gt | eq << 16) warp counts
   int32_t sel_bin;
   int32_t sel_krem;
+  int32_t sel_exact;
   int32_t first_drop;
   float red[kWarps * 4];
 };
@@ -79,6 +83,7 @@ __device__ void select_emit(const uint32_t* keys, int n, int K, int32_t* out, in
   }
   uint32_t prefix = 0, mask = 0;
   int krem = K;
+  bool exact = false;
   for (int i = tid; i < kRadixBins; i += kThreads) s.hist[0][i] = 0;
   G::sync();
 #pragma unroll 1
@@ -120,6 +125,7 @@ __device__ void select_emit(const uint32_t* keys, int n, int K, int32_t* out, in
           if (cum + c[b] >= (uint32_t)krem) {
             s.sel_bin = lane * per + b;
             s.sel_krem = krem - (int)cum;
+            s.sel_exact = (cum + c[b] == (uint32_t)krem) ? 1 : 0;  // the whole bin is kept
             break;
           }
           cum += c[b];
@@ -130,9 +136,16 @@ __device__ void select_emit(const uint32_t* keys, int n, int K, int32_t* out, in
     prefix |= (uint32_t)s.sel_bin << shift;
     mask |= 255u << shift;
     krem = s.sel_krem;
+    // Early exit: the boundary bin is kept whole, so the kept set is exactly
+    // {k : (k & mask) >= prefix} = {k : k >= prefix} -- no need to resolve the
+    // lower digits (prefix >= 1 here because K < n).
+    if (FC_SEL_EXACT && s.sel_exact) {
+      exact = true;
+      break;
+    }
   }
-  const uint32_t tau = prefix;
-  const int need = krem;
+  const uint32_t tau = exact ? prefix - 1u : prefix;
+  const int need = exact ? 0 : krem;
   // Emission in super-tiles of kEmitR x 256 keys (warp w owns kEmitR x 32
   // consecutive keys, one ballot per 32): one barrier per super-tile.
   constexpr int kEmitR = 4;
