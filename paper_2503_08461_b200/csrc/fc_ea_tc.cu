@@ -518,7 +518,7 @@ bool ea_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T,
   if ((dtype != FC_F16 && dtype != FC_BF16) || g.D != kD) return false;
   if (pp.num_q_heads != g.H) return false;   // one query head per kv head
   if (g.bs < 8 || g.bs > 128) return false;
-  return plan(g.bs, max_T, max_K).total <= 227 * 1024;
+  return plan(g.bs, max_T, max_K).total <= kDynSmemBudget;
 }
 
 fc_status encode_rows(CUtensorMap* map, const void* base, int dtype, int D, uint64_t rows, int box_rows);

@@ -25,6 +25,9 @@
 namespace fc {
 
 constexpr int kMaxBatch = 128;      // requests per press launch (kernel-param descriptor)
+// Dynamic SMEM a persistent kernel may request: the 227-KB per-CTA opt-in limit
+// minus headroom for its static __shared__ scratch (select / barrier words).
+constexpr int kDynSmemBudget = 227 * 1024 - 4096;
 constexpr int kMaxAllocBatch = 512; // requests per pop/push launch
 
 // Geometry of a pool, passed by value to kernels.

@@ -100,7 +100,7 @@ __host__ __device__ inline TcSmem tc_smem_plan(int D, int bs, int max_T) {
   p.total = p.off_bar + (2 * kTcStages + 8 + 2 * kSlots) * 8 + 1024;
   // the compactors' cp.async ring (D * 2-byte rows, 4 x 32-rank chunks) when it fits
   const int cbuf = FC_SNAP_CBUFS * FC_SNAP_CRANKS * 2 * D * 2;
-  p.async_compact = FC_SNAP_ASYNC_COMPACT && p.off_cbuf + cbuf + 1024 <= 227 * 1024;
+  p.async_compact = FC_SNAP_ASYNC_COMPACT && p.off_cbuf + cbuf + 1024 <= kDynSmemBudget;
   if (p.async_compact) p.total = p.off_cbuf + cbuf + 1024;
   return p;
 }
@@ -495,7 +495,7 @@ bool snapkv_tc_supported(const Geom& g, int dtype, const PressParams& pp, int ma
   if (pp.window != 32) return false;               // one 32x32b.x32 TMEM load per tile
   if (g.bs < 8 || g.bs > 128) return false;
   if ((max_T + kTileM - 1) / kTileM > kSlots) return false;         // whole segment in TMEM
-  if (tc_smem_plan(g.D, g.bs, max_T).total > 227 * 1024) return false;
+  if (tc_smem_plan(g.D, g.bs, max_T).total > kDynSmemBudget) return false;
   return true;
 }
 
