@@ -23,10 +23,6 @@ namespace fc {
 
 constexpr int kDecodeWarps = 4;
 constexpr int kDecodeThreads = kDecodeWarps * 32;
-constexpr int kMaxGq = 8;
-#ifndef FC_DECODE_PF  // L2 prefetch distance in tiles; measured slower at c2d (85 vs 70 us)
-#define FC_DECODE_PF 0
-#endif
 
 // The lane-group geometry of a row: kVpr 16-B vectors per row, kRows rows per
 // warp-wide load, kTile row-groups in flight per lane.
@@ -108,22 +104,6 @@ __global__ void __launch_bounds__(kDecodeThreads, G == 1 ? FC_DEC_MINB1 : 1)
   constexpr int kTileTok = kTile * kRows;
   constexpr int kStride = kDecodeWarps * kTileTok;
   for (int t0 = t_begin + warp * kTileTok; t0 < t_end; t0 += kStride) {
-#if FC_DECODE_PF > 0
-    // pull this warp's rows FC_DECODE_PF tiles ahead towards L2 (no registers held)
-    if (vec == 0) {
-      const int tp0 = t0 + FC_DECODE_PF * kStride;
-#pragma unroll
-      for (int u = 0; u < kTile; ++u) {
-        const int t = tp0 + u * kRows + sub;
-        if (t < t_end) {
-          const char* p = kbase + (int64_t)row_tab[t >> g.bs_shift] * g.block_stride +
-                          (int64_t)(t & (g.bs - 1)) * g.row_bytes;
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((int)g.row_bytes) : "memory");
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + v_off), "r"((int)g.row_bytes) : "memory");
-        }
-      }
-    }
-#endif
     uint4 kr[kTile], vr[kTile];
 #pragma unroll
     for (int u = 0; u < kTile; ++u) {
