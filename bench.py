@@ -43,6 +43,8 @@ CONFIGS = {
           "batch 32, Knorm 50%, fp16",
     "c3": "LLaVA-1.5-7B-shaped KV batch 64, SnapKV (window 32, pool 7) at 25% keep, "
           "variable-length requests (576 img + text U[64,960])",
+    "c3l": "SnapKV (window 32, pool 7) at 25% keep on c4w's 64 mixed-length requests (1k-8k "
+           "tokens): segments beyond the 2048-token TMEM ring take the two-pass tensor-core path",
     "c4w": "ExpectedAttention at 25% keep, 64 mixed-length requests (1k-8k tokens; one admission "
            "wave of config 4)",
     "c4": "ExpectedAttention at 25% keep on 256 mixed-length requests (1k-8k tokens) with pool "
@@ -57,7 +59,7 @@ CONFIGS = {
 }
 
 
-STRONG = {"c3", "c4w", "c4"}
+STRONG = {"c3", "c3l", "c4w", "c4"}
 
 
 def workload(name: str):
@@ -77,6 +79,12 @@ def workload(name: str):
         cfg = ModelConfig("llava-7b", 32, 32, 128, 2)
         txt = np.random.default_rng(0).integers(64, 961, 64)
         specs = [split_modalities(576, int(t)) for t in txt]
+        return cfg, "float16", specs, CompressorSpec(factor=4, press=PressKind.SNAPKV, window=32,
+                                                      pool_kernel=7)
+    if name == "c3l":
+        cfg = ModelConfig("llava-7b", 32, 32, 128, 2)
+        lens = np.random.default_rng(0).integers(1024, 8193, 256)[:64]
+        specs = [split_modalities(576, int(t) - 576) for t in lens]
         return cfg, "float16", specs, CompressorSpec(factor=4, press=PressKind.SNAPKV, window=32,
                                                       pool_kernel=7)
     if name in ("c4w", "c4"):

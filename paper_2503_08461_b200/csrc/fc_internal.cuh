@@ -197,7 +197,7 @@ fc_status launch_press(const Geom& g, int dtype, char* arena, const int32_t* src
                        int32_t* dst_table, const PressBatch& batch, const PressParams& pp,
                        const fc_press_inputs* in, const fc_press_outputs* out, float* workspace,
                        int64_t workspace_floats, int32_t* d_err, cudaStream_t stream);
-bool snapkv_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T);
+bool snapkv_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T, int max_K);
 fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t* table,
                            const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
                            const fc_press_outputs& out, cudaStream_t stream);

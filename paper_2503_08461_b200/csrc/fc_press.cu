@@ -591,8 +591,12 @@ static fc_status launch_one(const Geom& g, char* arena, const int32_t* src, int3
     note_launch();
     return cuda_check(cudaGetLastError(), "chunk_pool_kernel");
   }
-  if (KIND == FC_PRESS_SNAPKV && b.in_place && snapkv_tc_supported(g, Elem<T>::kDtype, pp, b.max_T))
-    return launch_snapkv_tc(g, Elem<T>::kDtype, arena, src, b, pp, in, out, stream);
+  if (KIND == FC_PRESS_SNAPKV && b.in_place) {
+    int max_K = 1;
+    for (int i = 0; i < b.n; ++i) max_K = max_K > b.req[i].K ? max_K : b.req[i].K;
+    if (snapkv_tc_supported(g, Elem<T>::kDtype, pp, b.max_T, max_K))
+      return launch_snapkv_tc(g, Elem<T>::kDtype, arena, src, b, pp, in, out, stream);
+  }
   if (KIND == FC_PRESS_EXPECTED_ATTENTION && b.in_place) {
     int max_K = 1;
     for (int i = 0; i < b.n; ++i) max_K = max_K > b.req[i].K ? max_K : b.req[i].K;

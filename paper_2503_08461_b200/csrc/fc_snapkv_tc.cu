@@ -83,7 +83,9 @@ struct TcSmem {
   bool async_compact;
 };
 
-__host__ __device__ inline TcSmem tc_smem_plan(int D, int bs, int max_T) {
+__host__ __device__ inline int snap_k_stride(int max_K) { return ((max_K * 4 + 15) & ~15) / 4; }
+
+__host__ __device__ inline TcSmem tc_smem_plan(int D, int bs, int max_T, int max_K) {
   TcSmem p;
   p.tile_bytes = kTileM * D * 2;
   p.q_bytes = (kWin * D * 2 + 1023) & ~1023;
@@ -92,10 +94,10 @@ __host__ __device__ inline TcSmem tc_smem_plan(int D, int bs, int max_T) {
   p.off_q = p.off_stage + kTcStages * p.tile_bytes;
   p.off_ptab = p.off_q + 2 * p.q_bytes;
   p.off_ctab = p.off_ptab + ((p.max_nb * 4 + 15) & ~15);          // [2][max_nb]
-  p.off_idx = p.off_ctab + 2 * ((p.max_nb * 4 + 15) & ~15);        // [2][max_T]
-  p.off_sc = p.off_idx + 2 * ((max_T * 4 + 15) & ~15);
-  p.off_s1 = p.off_sc + ((max_T * 4 + 15) & ~15);
-  p.off_bar = p.off_s1 + 2 * ((max_T * 4 + 15) & ~15);
+  p.off_idx = p.off_ctab + 2 * ((p.max_nb * 4 + 15) & ~15);        // [2][max_K] kept positions
+  p.off_sc = p.off_idx + 2 * snap_k_stride(max_K) * 4;
+  p.off_s1 = p.off_sc + ((max_T * 4 + 15) & ~15);                   // [8 zeros][max_T]
+  p.off_bar = p.off_s1 + (((max_T + 8) * 4 + 15) & ~15);
   p.off_cbuf = p.off_bar + (((2 * kTcStages + 8 + 2 * kSlots) * 8 + 127) & ~127);
   p.total = p.off_bar + (2 * kTcStages + 8 + 2 * kSlots) * 8 + 1024;
   // the compactors' cp.async ring (D * 2-byte rows, 4 x 32-rank chunks) when it fits
@@ -111,7 +113,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                      const __grid_constant__ PressBatch b, const PressParams pp,
                      const __grid_constant__ CUtensorMap kmap,
                      const __grid_constant__ CUtensorMap qmap, const fc_press_outputs out,
-                     int n_items) {
+                     int n_items, int max_K) {
   constexpr int kHalves = D / 64;  // 128-byte K-dim slabs
   constexpr int kKSteps = D / 16;  // UMMA_K = 16 for 16-bit inputs
   constexpr int kFmt = Elem<T>::kDtype == FC_BF16 ? 1 : 0;
@@ -120,23 +122,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __shared__ uint32_t s_tmem;
   __shared__ float s_red[kWarps][16];
   __shared__ float s_m[kWin], s_zinv[kWin];
+  __shared__ float s_zpart[kWarps][16];
 
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  const TcSmem plan = tc_smem_plan(D, g.bs, b.max_T);
+  const TcSmem plan = tc_smem_plan(D, g.bs, b.max_T, max_K);
   unsigned char* stages = smem + plan.off_stage;
   unsigned char* qbuf = smem + plan.off_q;
   int32_t* ptab = reinterpret_cast<int32_t*>(smem + plan.off_ptab);
   const int nb_stride = ((plan.max_nb * 4 + 15) & ~15) / 4;
-  const int t_stride = ((b.max_T * 4 + 15) & ~15) / 4;
+  const int k_stride = snap_k_stride(max_K);
   int32_t* ctab = reinterpret_cast<int32_t*>(smem + plan.off_ctab);   // [2][nb_stride]
-  int32_t* idxbuf = reinterpret_cast<int32_t*>(smem + plan.off_idx);  // [2][t_stride]
+  int32_t* idxbuf = reinterpret_cast<int32_t*>(smem + plan.off_idx);  // [2][k_stride]
   __shared__ CompactJob s_job[2];
   float* sc = reinterpret_cast<float*>(smem + plan.off_sc);
   // window means, front-padded with 8 zeros so the pooling window needs no bounds
-  // (the plan reserves 2 * max_T floats; one padded array uses max_T + 8)
   float* s1 = reinterpret_cast<float*>(smem + plan.off_s1) + 8;
-  const int s1_stride = ((b.max_T * 4 + 15) & ~15) / 4;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + plan.off_bar);
   uint64_t* st_full = bars;
   uint64_t* st_empty = bars + kTcStages;
@@ -184,13 +185,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       // K tiles: lane c issues chunk c's boxes (one round of issue per tile)
       const int64_t row_l = (int64_t)l * g.num_blocks * 2 * g.H * g.bs + (int64_t)h * g.bs;
-      for (int k = 0; k < ntiles; ++k, ++gtile) {
+      // a segment longer than the TMEM ring (T > kSlots * 128) is streamed twice:
+      // pass A (softmax statistics) and pass B (normalised window mean)
+      const int nload = ntiles > kSlots ? 2 * ntiles : ntiles;
+      for (int kl = 0; kl < nload; ++kl, ++gtile) {
+        const int k = kl < ntiles ? kl : kl - ntiles;
         const int st = gtile % kTcStages;
         const int n_chunks = min(chunks, nb - k * chunks);
         if (lane == 0) {
           tc::mbar_wait(&st_empty[st], ((gtile / kTcStages) & 1) ^ 1);
-          if (k == 0) FC_STAMP(it, 0);
-          if (k == ntiles - 1) FC_STAMP(it, 1);
+          if (kl == 0) FC_STAMP(it, 0);
+          if (kl == ntiles - 1) FC_STAMP(it, 1);
           tc::mbar_expect_tx(&st_full[st], (uint32_t)(n_chunks * g.bs * D * 2));
         }
         __syncwarp();
@@ -215,7 +220,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int qb = it & 1;
         tc::mbar_wait(&q_full[qb], (it >> 1) & 1);
         const uint32_t q_base = tc::smem_u32(qbuf + qb * plan.q_bytes);
-        for (int k = 0; k < ntiles; ++k, ++gtile) {
+        const int nload = ntiles > kSlots ? 2 * ntiles : ntiles;
+        for (int k = 0; k < nload; ++k, ++gtile) {
           const int st = gtile % kTcStages, sl = gtile % kSlots;
           tc::mbar_wait(&sl_empty[sl], ((gtile / kSlots) & 1) ^ 1);
           tc::mbar_wait(&st_full[st], (gtile / kTcStages) & 1);
@@ -247,11 +253,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #ifndef FC_NO_COMPACT
       if (plan.async_compact)
         compact_rows_async<D * (int)sizeof(T), Compactors, FC_SNAP_CRANKS, FC_SNAP_CBUFS>(
-            seg, g, ctab + jb * nb_stride, ctab + jb * nb_stride, idxbuf + jb * t_stride, job.K,
+            seg, g, ctab + jb * nb_stride, ctab + jb * nb_stride, idxbuf + jb * k_stride, job.K,
             job.first_moved, smem + plan.off_cbuf);
       else
         compact_rows<D * (int)sizeof(T), Compactors, 8>(seg, g, ctab + jb * nb_stride,
-                                                     ctab + jb * nb_stride, idxbuf + jb * t_stride,
+                                                     ctab + jb * nb_stride, idxbuf + jb * k_stride,
                                                      job.K, job.first_moved);
 #endif
       Compactors::sync();
@@ -283,6 +289,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       float acc[16];
       // s1 = the window mean of both query groups (pass 3 adds into it)
       for (int t = ct - 8; t < T_len; t += kThreads) s1[t] = 0.f;
+      if (ntiles <= kSlots) {
       // pass 1: per-query max over all tokens
 #pragma unroll
       for (int j = 0; j < 16; ++j) acc[j] = -INFINITY;
@@ -377,7 +384,96 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           atomicAdd(&s1[t], sum * (1.0f / (float)kWin));   // two addends onto 0: order-free
         }
       }
-      gtile += ntiles;
+      } else {
+        // ---- long segment (T > kSlots * 128): two streamed passes ----
+        // pass A: per-query running (reference max, sum of exp) as the tiles arrive,
+        // each TMEM slot freed at once. Lazy rescaling: the reference moves only when
+        // a logit exceeds it by more than 2^8, so the sum stays far from overflow.
+        float mref[16], ssum[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          mref[j] = -INFINITY;
+          ssum[j] = 0.f;
+        }
+        for (int k = 0; k < ntiles; ++k) {
+          const int sl = (gtile + k) % kSlots;
+          tc::mbar_wait(&sl_full[sl], ((gtile + k) / kSlots) & 1);
+          tc::fence_after_sync();
+          float v[16];
+          tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
+          const int t = k * kTileM + row;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (t < T_len && t <= T_len - kWin + grp * 16 + j) {
+              const float x = v[j] * scale;
+              if (x > mref[j] + 8.f) {
+                ssum[j] = (mref[j] == -INFINITY) ? 0.f : ssum[j] * tc::ex2(mref[j] - x);
+                mref[j] = x;
+              }
+              ssum[j] += tc::ex2(x - mref[j]);
+            }
+          }
+        }
+        // combine (reference max, sum) over the warp, then over the 4 lane quarters
+        float mw[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) mw[j] = mref[j];
+        const float mwarp = tc::warp_reduce16(mw, lane, [](float x, float y) { return fmaxf(x, y); });
+        // broadcast each query's warp max back (lanes 2q, 2q+1 hold query q)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float mj_w = __shfl_sync(0xffffffffu, mwarp, 2 * j);
+          ssum[j] = (mref[j] == -INFINITY) ? 0.f : ssum[j] * tc::ex2(mref[j] - mj_w);
+          mw[j] = mj_w;
+        }
+        const float swarp = tc::warp_reduce16(ssum, lane, [](float x, float y) { return x + y; });
+        if ((lane & 1) == 0) {
+          s_red[cw][lane >> 1] = mw[lane >> 1];
+          s_zpart[cw][lane >> 1] = swarp;
+        }
+        Consumers::sync();
+        if (ct < kWin) {
+          const int gg = ct >> 4, jj = ct & 15;
+          float m = s_red[4 * gg][jj];
+          for (int i = 1; i < 4; ++i) m = fmaxf(m, s_red[4 * gg + i][jj]);
+          float z = 0.f;
+          for (int i = 0; i < 4; ++i) {
+            const float mi = s_red[4 * gg + i][jj];
+            if (mi != -INFINITY) z += s_zpart[4 * gg + i][jj] * tc::ex2(mi - m);
+          }
+          s_m[ct] = m;
+          s_zinv[ct] = 1.0f / z;
+        }
+        Consumers::sync();
+        float mj[16], zj[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          mj[j] = s_m[grp * 16 + j];
+          zj[j] = s_zinv[grp * 16 + j];
+        }
+        // pass B: normalised probabilities of the re-streamed tiles -> window mean
+        for (int k = 0; k < ntiles; ++k) {
+          const int gk = gtile + ntiles + k, sl = gk % kSlots;
+          tc::mbar_wait(&sl_full[sl], (gk / kSlots) & 1);
+          tc::fence_after_sync();
+          float v[16];
+          tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
+          const int t = k * kTileM + row;
+          if (t < n_keep) {
+            float sum = 0.f;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sum = fmaf(tc::ex2(fmaf(v[j], scale, -mj[j])), zj[j], sum);
+            atomicAdd(&s1[t], sum * (1.0f / (float)kWin));   // two addends onto 0: order-free
+          }
+        }
+      }
+      gtile += ntiles > kSlots ? 2 * ntiles : ntiles;
       if (ct == 0) FC_STAMP(it, 4);
       Consumers::sync();
       // avg-pool (zero pad, count_include_pad), forced window
@@ -418,7 +514,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // hand the kept list to the compactors (double-buffered)
       tc::mbar_wait(&job_empty[jb], ((it >> 1) & 1) ^ 1);
       if (ct == 0) FC_STAMP(it, 13);
-      int32_t* idx = idxbuf + jb * t_stride;
+      int32_t* idx = idxbuf + jb * k_stride;
       for (int i = ct; i < nb; i += kThreads) ctab[jb * nb_stride + i] = table[(int64_t)q.slot * g.max_bpr + i];
       if (ct == 0) FC_STAMP(it, 14);
       if (b.per_segment && q.seg0 < T_len) {
@@ -483,7 +579,7 @@ fc_status encode_rows(CUtensorMap* map, const void* base, int dtype, int D, uint
   return FC_OK;
 }
 
-bool snapkv_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T) {
+bool snapkv_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T, int max_K) {
   static const bool forced_simt = [] {
     const char* e = getenv("FASTCACHE_SNAPKV_SIMT");
     return e && e[0] == '1';
@@ -494,8 +590,8 @@ bool snapkv_tc_supported(const Geom& g, int dtype, const PressParams& pp, int ma
   if (pp.num_q_heads != g.H) return false;          // one query head per kv head
   if (pp.window != 32) return false;               // one 32x32b.x32 TMEM load per tile
   if (g.bs < 8 || g.bs > 128) return false;
-  if ((max_T + kTileM - 1) / kTileM > kSlots) return false;         // whole segment in TMEM
-  if (tc_smem_plan(g.D, g.bs, max_T).total > kDynSmemBudget) return false;
+  // segments beyond the TMEM ring (T > kSlots * 128) take the two-pass path
+  if (tc_smem_plan(g.D, g.bs, max_T, max_K).total > kDynSmemBudget) return false;
   return true;
 }
 
@@ -510,7 +606,9 @@ fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t*
   st = encode_rows(&qmap, in.q_window, dtype, g.D,
                    (uint64_t)n_requests_total * g.L * pp.num_q_heads * pp.window, pp.window);
   if (st != FC_OK) return st;
-  const TcSmem plan = tc_smem_plan(g.D, g.bs, b.max_T);
+  int max_K = 1;
+  for (int i = 0; i < b.n; ++i) max_K = max_K > b.req[i].K ? max_K : b.req[i].K;
+  const TcSmem plan = tc_smem_plan(g.D, g.bs, b.max_T, max_K);
   const int n_items = b.n * g.L * g.H;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -519,7 +617,8 @@ fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t*
   auto launch = [&](auto kern) -> fc_status {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.total);
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(snapkv_tc)");
-    kern<<<grid, kTcThreads, plan.total, stream>>>(arena, table, g, b, pp, kmap, qmap, out, n_items);
+    kern<<<grid, kTcThreads, plan.total, stream>>>(arena, table, g, b, pp, kmap, qmap, out, n_items,
+                                                   max_K);
     note_launch();
     return cuda_check(cudaGetLastError(), "snapkv_tc_kernel");
   };
