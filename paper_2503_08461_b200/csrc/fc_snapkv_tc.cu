@@ -70,6 +70,9 @@ struct CompactJob {  // consumer -> compactor hand-off of one segment
 #ifndef FC_SNAP_ASYNC_COMPACT
 #define FC_SNAP_ASYNC_COMPACT 1
 #endif
+#ifndef FC_SNAP_L2HINT  // L2 eviction hints on the K tiles (evict-last for a long segment's pass A)
+#define FC_SNAP_L2HINT 1
+#endif
 #ifndef FC_SNAP_CRANKS
 #define FC_SNAP_CRANKS 32
 #endif
@@ -166,6 +169,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0) {
     // ================= TMA producer =================
     const int chunks = kTileM / g.bs;
+    const uint64_t pol_last = tc::l2_policy_evict_last(), pol_first = tc::l2_policy_evict_first();
     int gtile = 0;
     for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
       const int r = item / LH, lh = item % LH, l = lh / g.H, h = lh % g.H;
@@ -200,12 +204,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         __syncwarp();
         unsigned char* dst = stages + st * plan.tile_bytes;
+        // long segments: pass A asks L2 to keep the tiles (pass B re-reads them),
+        // pass B and short segments mark them evict-first (read once)
+        const uint64_t pol = (FC_SNAP_L2HINT && nload > ntiles && kl < ntiles) ? pol_last : pol_first;
         for (int c = lane; c < n_chunks; c += 32) {
           const int64_t row0 = row_l + (int64_t)ptab[k * chunks + c] * 2 * g.H * g.bs;
 #pragma unroll
-          for (int hf = 0; hf < kHalves; ++hf)
-            tc::tma_load_2d(dst + hf * kTileM * 128 + c * g.bs * 128, &kmap, &st_full[st],
-                            hf * 64, (int)row0);
+          for (int hf = 0; hf < kHalves; ++hf) {
+            if (FC_SNAP_L2HINT)
+              tc::tma_load_2d_hint(dst + hf * kTileM * 128 + c * g.bs * 128, &kmap, &st_full[st],
+                                   hf * 64, (int)row0, pol);
+            else
+              tc::tma_load_2d(dst + hf * kTileM * 128 + c * g.bs * 128, &kmap, &st_full[st],
+                              hf * 64, (int)row0);
+          }
         }
       }
     }
