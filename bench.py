@@ -45,6 +45,8 @@ CONFIGS = {
           "variable-length requests (576 img + text U[64,960])",
     "c3l": "SnapKV (window 32, pool 7) at 25% keep on c4w's 64 mixed-length requests (1k-8k "
            "tokens): segments beyond the 2048-token TMEM ring take the two-pass tensor-core path",
+    "c3g": "SnapKV (window 32, pool 7) at 25% keep with GQA: Llama-3-8B-shaped KV (32 layers, 8 kv "
+           "heads, 32 query heads, d=128), c3's 64 variable-length requests",
     "c4w": "ExpectedAttention at 25% keep, 64 mixed-length requests (1k-8k tokens; one admission "
            "wave of config 4)",
     "c4": "ExpectedAttention at 25% keep on 256 mixed-length requests (1k-8k tokens) with pool "
@@ -59,7 +61,8 @@ CONFIGS = {
 }
 
 
-STRONG = {"c3", "c3l", "c4w", "c4"}
+STRONG = {"c3", "c3g", "c3l", "c4w", "c4"}
+Q_HEADS = {"c3g": 32}   # query heads when they differ from the kv heads (GQA)
 
 
 def workload(name: str):
@@ -81,6 +84,12 @@ def workload(name: str):
         specs = [split_modalities(576, int(t)) for t in txt]
         return cfg, "float16", specs, CompressorSpec(factor=4, press=PressKind.SNAPKV, window=32,
                                                       pool_kernel=7)
+    if name == "c3g":
+        cfg = ModelConfig("llama-3-8b", 32, 8, 128, 2)
+        txt = np.random.default_rng(0).integers(64, 961, 64)
+        specs = [split_modalities(576, int(t)) for t in txt]
+        return cfg, "float16", specs, CompressorSpec(factor=4, press=PressKind.SNAPKV, window=32,
+                                                      pool_kernel=7)
     if name == "c3l":
         cfg = ModelConfig("llava-7b", 32, 32, 128, 2)
         lens = np.random.default_rng(0).integers(1024, 8193, 256)[:64]
@@ -97,13 +106,13 @@ def workload(name: str):
     raise SystemExit(f"unknown config {name}")
 
 
-def alg_bytes(cfg, specs, comp) -> int:
+def alg_bytes(cfg, specs, comp, hq=None) -> int:
     """SURVEY.md §8(d) algorithmic HBM bytes of one batch (R raw, C kept)."""
     from paper_2503_08461_b200 import PressKind, compressed_spec, kv_bytes
 
     raw = sum(kv_bytes(cfg, s.total_tokens) for s in specs)
     kept = sum(kv_bytes(cfg, compressed_spec(s, comp).total_tokens) for s in specs)
-    lhq = cfg.num_layers * cfg.num_kv_heads
+    lhq = cfg.num_layers * (hq or cfg.num_kv_heads)
     if comp.press is PressKind.KNORM:
         return raw // 2 + 2 * kept
     if comp.press is PressKind.SNAPKV:
@@ -182,12 +191,13 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def press_inputs(comp, cfg, n, device, torch, seed):
+def press_inputs(comp, cfg, n, device, torch, seed, hq=None):
     from paper_2503_08461_b200 import PressKind
 
+    hq = hq or cfg.num_kv_heads
     gen = torch.Generator(device=device).manual_seed(seed)
     if comp.press is PressKind.SNAPKV:
-        q = torch.randn((n, cfg.num_layers, cfg.num_kv_heads, comp.window, cfg.head_dim),
+        q = torch.randn((n, cfg.num_layers, hq, comp.window, cfg.head_dim),
                         generator=gen, device=device, dtype=torch.float32).half()
         return {"q_window": q}
     if comp.press is PressKind.EXPECTED_ATTENTION:
@@ -532,9 +542,10 @@ def run_ours(args, rank, world, local_rank):
     cap = sum(kv_bytes(cfg, s.total_tokens) for s in specs)
     pool = KVCachePool(cfg, cap, device=device, kv_dtype=dtype, max_handles=max(64, 2 * n),
                        max_tokens_per_handle=max(s.total_tokens for s in specs) + 64,
-                       num_q_heads=cfg.num_kv_heads)
+                       num_q_heads=Q_HEADS.get(args.config, cfg.num_kv_heads))
     pool.set_profiling(True)
-    ins = press_inputs(comp, cfg, n, device, torch, seed=1234 + rank)
+    ins = press_inputs(comp, cfg, n, device, torch, seed=1234 + rank,
+                       hq=Q_HEADS.get(args.config, cfg.num_kv_heads))
     rids = [rank * 1_000_000 + i for i in range(n)]
     stream = torch.cuda.current_stream(device)
 
@@ -571,7 +582,7 @@ def run_ours(args, rank, world, local_rank):
     total_ms = sum(step_ms)
     max_ms = _allreduce(total_ms, "max", device)
     value = job_tokens * args.steps / (max_ms / 1e3)
-    abytes = alg_bytes(cfg, specs, comp)
+    abytes = alg_bytes(cfg, specs, comp, Q_HEADS.get(args.config))
     peak, peak_kind = measured_peak()
     press_avg = statistics.mean(press_ms)
     achieved = abytes / (press_avg / 1e3) / 1e9

@@ -110,7 +110,7 @@ __host__ __device__ inline TcSmem tc_smem_plan(int D, int bs, int max_T, int max
   return p;
 }
 
-template <typename T, int D>
+template <typename T, int D, bool kGqa>
 __global__ void __launch_bounds__(kTcThreads, 1)
     snapkv_tc_kernel(char* __restrict__ arena, const int32_t* __restrict__ table, const Geom g,
                      const __grid_constant__ PressBatch b, const PressParams pp,
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ================= TMA producer =================
     const int chunks = kTileM / g.bs;
     const uint64_t pol_last = tc::l2_policy_evict_last(), pol_first = tc::l2_policy_evict_first();
-    int gtile = 0;
+    int gtile = 0, unit = 0;
     for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
       const int r = item / LH, lh = item % LH, l = lh / g.H, h = lh % g.H;
       const PressReq q = b.req[r];
@@ -178,45 +178,52 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       __syncwarp();
       for (int i = lane; i < nb; i += 32) ptab[i] = table[(int64_t)q.slot * g.max_bpr + i];
       __syncwarp();
-      if (lane == 0) {
-        const int qb = it & 1;
-        tc::mbar_wait(&q_empty[qb], ((it >> 1) & 1) ^ 1);
-        const int qrow = (int)((((int64_t)q.q_idx * g.L + l) * pp.num_q_heads + h) * kWin);
-        tc::mbar_expect_tx(&q_full[qb], (uint32_t)(kWin * D * 2));
-#pragma unroll
-        for (int hf = 0; hf < kHalves; ++hf)
-          tc::tma_load_2d(qbuf + qb * plan.q_bytes + hf * kWin * 128, &qmap, &q_full[qb], hf * 64, qrow);
-      }
-      // K tiles: lane c issues chunk c's boxes (one round of issue per tile)
+      // GQA: the gq query heads sharing this kv head are scored one after the
+      // other ("units"); the first gq - 1 passes over K ask L2 to keep the tiles
+      // so the repeats come from L2, not HBM.
+      const int gq = kGqa ? pp.num_q_heads / g.H : 1;
       const int64_t row_l = (int64_t)l * g.num_blocks * 2 * g.H * g.bs + (int64_t)h * g.bs;
       // a segment longer than the TMEM ring (T > kSlots * 128) is streamed twice:
       // pass A (softmax statistics) and pass B (normalised window mean)
       const int nload = ntiles > kSlots ? 2 * ntiles : ntiles;
-      for (int kl = 0; kl < nload; ++kl, ++gtile) {
-        const int k = kl < ntiles ? kl : kl - ntiles;
-        const int st = gtile % kTcStages;
-        const int n_chunks = min(chunks, nb - k * chunks);
+      for (int gi = 0; gi < gq; ++gi, ++unit) {
         if (lane == 0) {
-          tc::mbar_wait(&st_empty[st], ((gtile / kTcStages) & 1) ^ 1);
-          if (kl == 0) FC_STAMP(it, 0);
-          if (kl == ntiles - 1) FC_STAMP(it, 1);
-          tc::mbar_expect_tx(&st_full[st], (uint32_t)(n_chunks * g.bs * D * 2));
-        }
-        __syncwarp();
-        unsigned char* dst = stages + st * plan.tile_bytes;
-        // long segments: pass A asks L2 to keep the tiles (pass B re-reads them),
-        // pass B and short segments mark them evict-first (read once)
-        const uint64_t pol = (FC_SNAP_L2HINT && nload > ntiles && kl < ntiles) ? pol_last : pol_first;
-        for (int c = lane; c < n_chunks; c += 32) {
-          const int64_t row0 = row_l + (int64_t)ptab[k * chunks + c] * 2 * g.H * g.bs;
+          const int qb = unit & 1;
+          tc::mbar_wait(&q_empty[qb], ((unit >> 1) & 1) ^ 1);
+          const int qrow = (int)((((int64_t)q.q_idx * g.L + l) * pp.num_q_heads + h * gq + gi) * kWin);
+          tc::mbar_expect_tx(&q_full[qb], (uint32_t)(kWin * D * 2));
 #pragma unroll
-          for (int hf = 0; hf < kHalves; ++hf) {
-            if (FC_SNAP_L2HINT)
-              tc::tma_load_2d_hint(dst + hf * kTileM * 128 + c * g.bs * 128, &kmap, &st_full[st],
-                                   hf * 64, (int)row0, pol);
-            else
-              tc::tma_load_2d(dst + hf * kTileM * 128 + c * g.bs * 128, &kmap, &st_full[st],
-                              hf * 64, (int)row0);
+          for (int hf = 0; hf < kHalves; ++hf)
+            tc::tma_load_2d(qbuf + qb * plan.q_bytes + hf * kWin * 128, &qmap, &q_full[qb], hf * 64, qrow);
+        }
+        // K tiles: lane c issues chunk c's boxes (one round of issue per tile)
+        for (int kl = 0; kl < nload; ++kl, ++gtile) {
+          const int k = kl < ntiles ? kl : kl - ntiles;
+          const int st = gtile % kTcStages;
+          const int n_chunks = min(chunks, nb - k * chunks);
+          if (lane == 0) {
+            tc::mbar_wait(&st_empty[st], ((gtile / kTcStages) & 1) ^ 1);
+            if (gi == 0 && kl == 0) FC_STAMP(it, 0);
+            if (gi == 0 && kl == ntiles - 1) FC_STAMP(it, 1);
+            tc::mbar_expect_tx(&st_full[st], (uint32_t)(n_chunks * g.bs * D * 2));
+          }
+          __syncwarp();
+          unsigned char* dst = stages + st * plan.tile_bytes;
+          // evict-last while a later pass (pass B, or the next query head) re-reads
+          // the tile; evict-first on its last read
+          const bool reread = gi + 1 < gq || (nload > ntiles && kl < ntiles);
+          const uint64_t pol = (FC_SNAP_L2HINT && reread) ? pol_last : pol_first;
+          for (int c = lane; c < n_chunks; c += 32) {
+            const int64_t row0 = row_l + (int64_t)ptab[k * chunks + c] * 2 * g.H * g.bs;
+#pragma unroll
+            for (int hf = 0; hf < kHalves; ++hf) {
+              if (FC_SNAP_L2HINT)
+                tc::tma_load_2d_hint(dst + hf * kTileM * 128 + c * g.bs * 128, &kmap, &st_full[st],
+                                     hf * 64, (int)row0, pol);
+              else
+                tc::tma_load_2d(dst + hf * kTileM * 128 + c * g.bs * 128, &kmap, &st_full[st],
+                                hf * 64, (int)row0);
+            }
           }
         }
       }
@@ -225,12 +232,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ================= MMA issuer =================
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_f16(kFmt, kTileM, kWin);
-      int gtile = 0;
+      int gtile = 0, unit = 0;
+      const int gq = kGqa ? pp.num_q_heads / g.H : 1;
       for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
         const PressReq q = b.req[item / LH];
         const int ntiles = (q.T + kTileM - 1) / kTileM;
-        const int qb = it & 1;
-        tc::mbar_wait(&q_full[qb], (it >> 1) & 1);
+        for (int gi = 0; gi < gq; ++gi, ++unit) {
+        const int qb = unit & 1;
+        tc::mbar_wait(&q_full[qb], (unit >> 1) & 1);
         const uint32_t q_base = tc::smem_u32(qbuf + qb * plan.q_bytes);
         const int nload = ntiles > kSlots ? 2 * ntiles : ntiles;
         for (int k = 0; k < nload; ++k, ++gtile) {
@@ -250,6 +259,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           tc::mma_commit(&sl_full[sl]);
         }
         tc::mma_commit(&q_empty[qb]);
+        }
         FC_STAMP(it, 2);
       }
     }
@@ -301,176 +311,95 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       float acc[16];
       // s1 = the window mean of both query groups (pass 3 adds into it)
       for (int t = ct - 8; t < T_len; t += kThreads) s1[t] = 0.f;
-      if (ntiles <= kSlots) {
-      // pass 1: per-query max over all tokens
-#pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = -INFINITY;
-      for (int k = 0; k < ntiles; ++k) {
-        const int sl = (gtile + k) % kSlots;
-        tc::mbar_wait(&sl_full[sl], ((gtile + k) / kSlots) & 1);
-        tc::fence_after_sync();
-        float v[16];
-        tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
-        const int t = k * kTileM + row;
-        if (t <= T_len - kWin) {   // below the window: no causal mask
-#pragma unroll
-          for (int j = 0; j < 16; ++j) acc[j] = fmaxf(acc[j], v[j] * scale);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (t < T_len && t <= T_len - kWin + grp * 16 + j) acc[j] = fmaxf(acc[j], v[j] * scale);
-        }
-      }
-      if (ct == 0) FC_STAMP(it, 3);
-      {
-        const float r = tc::warp_reduce16(acc, lane, [](float a, float b) { return fmaxf(a, b); });
-        if ((lane & 1) == 0) s_red[cw][lane >> 1] = r;
-      }
-      Consumers::sync();
-      if (ct < kWin) {
-        const int gg = ct >> 4, jj = ct & 15;
-        float m = s_red[4 * gg][jj];
-        for (int i = 1; i < 4; ++i) m = fmaxf(m, s_red[4 * gg + i][jj]);
-        s_m[ct] = m;
-      }
-      Consumers::sync();
-      float mj[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) mj[j] = s_m[grp * 16 + j];
-      if (ct == 0) FC_STAMP(it, 8);
-      // pass 2: per-query sum of exp
-#pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-      for (int k = 0; k < ntiles; ++k) {
-        const int sl = (gtile + k) % kSlots;
-        float v[16];
-        tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
-        const int t = k * kTileM + row;
-        if (t <= T_len - kWin) {   // below the window: no causal mask
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            v[j] = tc::ex2(fmaf(v[j], scale, -mj[j]));
-            acc[j] += v[j];
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float e = (t < T_len && t <= T_len - kWin + grp * 16 + j) ? tc::ex2(fmaf(v[j], scale, -mj[j])) : 0.f;
-            acc[j] += e;
-            v[j] = e;
-          }
-        }
-        tc::tmem_st_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);   // exps replace the logits
-      }
-      tc::tmem_store_wait();
-      if (ct == 0) FC_STAMP(it, 9);
-      {
-        const float r = tc::warp_reduce16(acc, lane, [](float a, float b) { return a + b; });
-        if ((lane & 1) == 0) s_red[cw][lane >> 1] = r;
-      }
-      Consumers::sync();
-      if (ct < kWin) {
-        const int gg = ct >> 4, jj = ct & 15;
-        float z = 0.f;
-        for (int i = 0; i < 4; ++i) z += s_red[4 * gg + i][jj];
-        s_zinv[ct] = 1.0f / z;
-      }
-      Consumers::sync();
-      float zj[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) zj[j] = s_zinv[grp * 16 + j];
-      if (ct == 0) FC_STAMP(it, 10);
-      // pass 3: partial window mean of the normalised probabilities; frees TMEM slots
-      for (int k = 0; k < ntiles; ++k) {
-        const int sl = (gtile + k) % kSlots;
-        float v[16];
-        tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
-        const int t = k * kTileM + row;
-        if (t < n_keep) {
-          float sum = 0.f;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) sum = fmaf(v[j], zj[j], sum);   // masked entries are 0
-          atomicAdd(&s1[t], sum * (1.0f / (float)kWin));   // two addends onto 0: order-free
-        }
-      }
-      } else {
-        // ---- long segment (T > kSlots * 128): two streamed passes ----
-        // pass A: per-query running (reference max, sum of exp) as the tiles arrive,
-        // each TMEM slot freed at once. Lazy rescaling: the reference moves only when
-        // a logit exceeds it by more than 2^8, so the sum stays far from overflow.
-        float mref[16], ssum[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          mref[j] = -INFINITY;
-          ssum[j] = 0.f;
-        }
+      // GQA: one unit per query head of the group; each adds its window mean
+      // (weighted 1/(w * gq)) into s1 -- for gq = 1 the two groups' addends land
+      // on 0 (order-free), for gq > 1 the float atomics may differ in the last ulp
+      // from run to run
+      const int gq = kGqa ? pp.num_q_heads / g.H : 1;
+      const float inv_wg = 1.0f / (float)(kWin * gq);
+      for (int gi = 0; gi < gq; ++gi) {
+        if (ntiles <= kSlots) {
+        // pass 1: per-query max over all tokens
+  #pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = -INFINITY;
         for (int k = 0; k < ntiles; ++k) {
           const int sl = (gtile + k) % kSlots;
           tc::mbar_wait(&sl_full[sl], ((gtile + k) / kSlots) & 1);
           tc::fence_after_sync();
           float v[16];
           tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
           const int t = k * kTileM + row;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (t < T_len && t <= T_len - kWin + grp * 16 + j) {
-              const float x = v[j] * scale;
-              if (x > mref[j] + 8.f) {
-                ssum[j] = (mref[j] == -INFINITY) ? 0.f : ssum[j] * tc::ex2(mref[j] - x);
-                mref[j] = x;
-              }
-              ssum[j] += tc::ex2(x - mref[j]);
-            }
+          if (t <= T_len - kWin) {   // below the window: no causal mask
+  #pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] = fmaxf(acc[j], v[j] * scale);
+          } else {
+  #pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (t < T_len && t <= T_len - kWin + grp * 16 + j) acc[j] = fmaxf(acc[j], v[j] * scale);
           }
         }
-        // combine (reference max, sum) over the warp, then over the 4 lane quarters
-        float mw[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) mw[j] = mref[j];
-        const float mwarp = tc::warp_reduce16(mw, lane, [](float x, float y) { return fmaxf(x, y); });
-        // broadcast each query's warp max back (lanes 2q, 2q+1 hold query q)
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float mj_w = __shfl_sync(0xffffffffu, mwarp, 2 * j);
-          ssum[j] = (mref[j] == -INFINITY) ? 0.f : ssum[j] * tc::ex2(mref[j] - mj_w);
-          mw[j] = mj_w;
-        }
-        const float swarp = tc::warp_reduce16(ssum, lane, [](float x, float y) { return x + y; });
-        if ((lane & 1) == 0) {
-          s_red[cw][lane >> 1] = mw[lane >> 1];
-          s_zpart[cw][lane >> 1] = swarp;
+        if (ct == 0) FC_STAMP(it, 3);
+        {
+          const float r = tc::warp_reduce16(acc, lane, [](float a, float b) { return fmaxf(a, b); });
+          if ((lane & 1) == 0) s_red[cw][lane >> 1] = r;
         }
         Consumers::sync();
         if (ct < kWin) {
           const int gg = ct >> 4, jj = ct & 15;
           float m = s_red[4 * gg][jj];
           for (int i = 1; i < 4; ++i) m = fmaxf(m, s_red[4 * gg + i][jj]);
-          float z = 0.f;
-          for (int i = 0; i < 4; ++i) {
-            const float mi = s_red[4 * gg + i][jj];
-            if (mi != -INFINITY) z += s_zpart[4 * gg + i][jj] * tc::ex2(mi - m);
-          }
           s_m[ct] = m;
+        }
+        Consumers::sync();
+        float mj[16];
+  #pragma unroll
+        for (int j = 0; j < 16; ++j) mj[j] = s_m[grp * 16 + j];
+        if (ct == 0) FC_STAMP(it, 8);
+        // pass 2: per-query sum of exp
+  #pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+        for (int k = 0; k < ntiles; ++k) {
+          const int sl = (gtile + k) % kSlots;
+          float v[16];
+          tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+          const int t = k * kTileM + row;
+          if (t <= T_len - kWin) {   // below the window: no causal mask
+  #pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              v[j] = tc::ex2(fmaf(v[j], scale, -mj[j]));
+              acc[j] += v[j];
+            }
+          } else {
+  #pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float e = (t < T_len && t <= T_len - kWin + grp * 16 + j) ? tc::ex2(fmaf(v[j], scale, -mj[j])) : 0.f;
+              acc[j] += e;
+              v[j] = e;
+            }
+          }
+          tc::tmem_st_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);   // exps replace the logits
+        }
+        tc::tmem_store_wait();
+        if (ct == 0) FC_STAMP(it, 9);
+        {
+          const float r = tc::warp_reduce16(acc, lane, [](float a, float b) { return a + b; });
+          if ((lane & 1) == 0) s_red[cw][lane >> 1] = r;
+        }
+        Consumers::sync();
+        if (ct < kWin) {
+          const int gg = ct >> 4, jj = ct & 15;
+          float z = 0.f;
+          for (int i = 0; i < 4; ++i) z += s_red[4 * gg + i][jj];
           s_zinv[ct] = 1.0f / z;
         }
         Consumers::sync();
-        float mj[16], zj[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          mj[j] = s_m[grp * 16 + j];
-          zj[j] = s_zinv[grp * 16 + j];
-        }
-        // pass B: normalised probabilities of the re-streamed tiles -> window mean
+        float zj[16];
+  #pragma unroll
+        for (int j = 0; j < 16; ++j) zj[j] = s_zinv[grp * 16 + j];
+        if (ct == 0) FC_STAMP(it, 10);
+        // pass 3: partial window mean of the normalised probabilities; frees TMEM slots
         for (int k = 0; k < ntiles; ++k) {
-          const int gk = gtile + ntiles + k, sl = gk % kSlots;
-          tc::mbar_wait(&sl_full[sl], (gk / kSlots) & 1);
-          tc::fence_after_sync();
+          const int sl = (gtile + k) % kSlots;
           float v[16];
           tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
           tc::fence_before_sync();
@@ -479,13 +408,102 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const int t = k * kTileM + row;
           if (t < n_keep) {
             float sum = 0.f;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) sum = fmaf(tc::ex2(fmaf(v[j], scale, -mj[j])), zj[j], sum);
-            atomicAdd(&s1[t], sum * (1.0f / (float)kWin));   // two addends onto 0: order-free
+  #pragma unroll
+            for (int j = 0; j < 16; ++j) sum = fmaf(v[j], zj[j], sum);   // masked entries are 0
+            atomicAdd(&s1[t], sum * inv_wg);
           }
         }
+        } else {
+          // ---- long segment (T > kSlots * 128): two streamed passes ----
+          // pass A: per-query running (reference max, sum of exp) as the tiles arrive,
+          // each TMEM slot freed at once. Lazy rescaling: the reference moves only when
+          // a logit exceeds it by more than 2^8, so the sum stays far from overflow.
+          float mref[16], ssum[16];
+  #pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            mref[j] = -INFINITY;
+            ssum[j] = 0.f;
+          }
+          for (int k = 0; k < ntiles; ++k) {
+            const int sl = (gtile + k) % kSlots;
+            tc::mbar_wait(&sl_full[sl], ((gtile + k) / kSlots) & 1);
+            tc::fence_after_sync();
+            float v[16];
+            tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
+            const int t = k * kTileM + row;
+  #pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (t < T_len && t <= T_len - kWin + grp * 16 + j) {
+                const float x = v[j] * scale;
+                if (x > mref[j] + 8.f) {
+                  ssum[j] = (mref[j] == -INFINITY) ? 0.f : ssum[j] * tc::ex2(mref[j] - x);
+                  mref[j] = x;
+                }
+                ssum[j] += tc::ex2(x - mref[j]);
+              }
+            }
+          }
+          // combine (reference max, sum) over the warp, then over the 4 lane quarters
+          float mw[16];
+  #pragma unroll
+          for (int j = 0; j < 16; ++j) mw[j] = mref[j];
+          const float mwarp = tc::warp_reduce16(mw, lane, [](float x, float y) { return fmaxf(x, y); });
+          // broadcast each query's warp max back (lanes 2q, 2q+1 hold query q)
+  #pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float mj_w = __shfl_sync(0xffffffffu, mwarp, 2 * j);
+            ssum[j] = (mref[j] == -INFINITY) ? 0.f : ssum[j] * tc::ex2(mref[j] - mj_w);
+            mw[j] = mj_w;
+          }
+          const float swarp = tc::warp_reduce16(ssum, lane, [](float x, float y) { return x + y; });
+          if ((lane & 1) == 0) {
+            s_red[cw][lane >> 1] = mw[lane >> 1];
+            s_zpart[cw][lane >> 1] = swarp;
+          }
+          Consumers::sync();
+          if (ct < kWin) {
+            const int gg = ct >> 4, jj = ct & 15;
+            float m = s_red[4 * gg][jj];
+            for (int i = 1; i < 4; ++i) m = fmaxf(m, s_red[4 * gg + i][jj]);
+            float z = 0.f;
+            for (int i = 0; i < 4; ++i) {
+              const float mi = s_red[4 * gg + i][jj];
+              if (mi != -INFINITY) z += s_zpart[4 * gg + i][jj] * tc::ex2(mi - m);
+            }
+            s_m[ct] = m;
+            s_zinv[ct] = 1.0f / z;
+          }
+          Consumers::sync();
+          float mj[16], zj[16];
+  #pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            mj[j] = s_m[grp * 16 + j];
+            zj[j] = s_zinv[grp * 16 + j];
+          }
+          // pass B: normalised probabilities of the re-streamed tiles -> window mean
+          for (int k = 0; k < ntiles; ++k) {
+            const int gk = gtile + ntiles + k, sl = gk % kSlots;
+            tc::mbar_wait(&sl_full[sl], (gk / kSlots) & 1);
+            tc::fence_after_sync();
+            float v[16];
+            tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
+            const int t = k * kTileM + row;
+            if (t < n_keep) {
+              float sum = 0.f;
+  #pragma unroll
+              for (int j = 0; j < 16; ++j) sum = fmaf(tc::ex2(fmaf(v[j], scale, -mj[j])), zj[j], sum);
+              atomicAdd(&s1[t], sum * inv_wg);
+            }
+          }
+        }
+        gtile += ntiles > kSlots ? 2 * ntiles : ntiles;
       }
-      gtile += ntiles > kSlots ? 2 * ntiles : ntiles;
       if (ct == 0) FC_STAMP(it, 4);
       Consumers::sync();
       // avg-pool (zero pad, count_include_pad), forced window
@@ -599,7 +617,7 @@ bool snapkv_tc_supported(const Geom& g, int dtype, const PressParams& pp, int ma
   if (forced_simt) return false;
   if (dtype != FC_F16 && dtype != FC_BF16) return false;
   if (g.D != 64 && g.D != 128) return false;
-  if (pp.num_q_heads != g.H) return false;          // one query head per kv head
+  if (pp.num_q_heads % g.H != 0 || pp.num_q_heads / g.H > 8) return false;   // GQA: gq <= 8
   if (pp.window != 32) return false;               // one 32x32b.x32 TMEM load per tile
   if (g.bs < 8 || g.bs > 128) return false;
   // segments beyond the TMEM ring (T > kSlots * 128) take the two-pass path
@@ -634,9 +652,14 @@ fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t*
     note_launch();
     return cuda_check(cudaGetLastError(), "snapkv_tc_kernel");
   };
-  if (dtype == FC_BF16)
-    return g.D == 64 ? launch(snapkv_tc_kernel<__nv_bfloat16, 64>) : launch(snapkv_tc_kernel<__nv_bfloat16, 128>);
-  return g.D == 64 ? launch(snapkv_tc_kernel<__half, 64>) : launch(snapkv_tc_kernel<__half, 128>);
+  // g = 1 gets its own instantiation (the unit loop folds away)
+  const bool gqa = pp.num_q_heads != g.H;
+  if (dtype == FC_BF16) {
+    if (g.D == 64) return gqa ? launch(snapkv_tc_kernel<__nv_bfloat16, 64, true>) : launch(snapkv_tc_kernel<__nv_bfloat16, 64, false>);
+    return gqa ? launch(snapkv_tc_kernel<__nv_bfloat16, 128, true>) : launch(snapkv_tc_kernel<__nv_bfloat16, 128, false>);
+  }
+  if (g.D == 64) return gqa ? launch(snapkv_tc_kernel<__half, 64, true>) : launch(snapkv_tc_kernel<__half, 64, false>);
+  return gqa ? launch(snapkv_tc_kernel<__half, 128, true>) : launch(snapkv_tc_kernel<__half, 128, false>);
 }
 
 }  // namespace fc

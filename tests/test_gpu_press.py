@@ -217,6 +217,8 @@ def _snap_inputs(n, L, hq, w, D, seed, device, dtype):
     ("float16", 2, 3, 1, 64, [(300, 17), (129, 0)], 32, 5),                # tcgen05, D=64
     ("float16", 1, 2, 1, 128, [(576, 2500), (0, 100), (1, 8000)], 32, 7),  # tcgen05, T > 2048: two passes
     ("bfloat16", 1, 1, 1, 128, [(0, 2049), (576, 1472)], 32, 7),           # tcgen05, 17 vs 16 tiles
+    ("float16", 2, 2, 4, 128, [(576, 200), (0, 900), (1, 2500)], 32, 7),    # tcgen05 GQA g=4 (+ long)
+    ("bfloat16", 1, 4, 2, 64, [(0, 300), (100, 1000)], 32, 7),             # tcgen05 GQA g=2, D=64
     ("bfloat16", 1, 2, 2, 64, [(0, 300), (100, 21)], 16, 5),
     ("float32", 1, 1, 4, 128, [(50, 50)], 8, 3),
 ])
