@@ -525,7 +525,7 @@ def run_prefill_bench(args, rank, world, local_rank):
 def run_ours(args, rank, world, local_rank):
     import torch
 
-    from paper_2503_08461_b200 import KVCachePool, _native, kv_bytes
+    from paper_2503_08461_b200 import KVCachePool, _native, compressed_spec, kv_bytes
 
     from paper_2503_08461_b200 import shard
 
@@ -609,6 +609,8 @@ def run_ours(args, rank, world, local_rank):
             "timing": "CUDA events on the launch stream around compress_batch, summed over steps",
         },
         "hbm_gbs_per_gpu": abytes * args.steps / (max_ms / 1e3) / 1e9,
+        "kept_tokens_per_s": (sum(compressed_spec(s, comp).total_tokens for s in specs) * world
+                              * args.steps / (max_ms / 1e3)),
         "roofline": {
             "bound": "hbm", "kernel": "press_kernel (score + top-k + in-place compaction)",
             "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
