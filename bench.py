@@ -533,6 +533,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(device)
     cfg, dtype, specs, comp = workload(args.config)
     strong = args.config in STRONG
+    job_kept = sum(compressed_spec(s, comp).total_tokens for s in specs) * (1 if strong else world)
     if strong:  # fixed total work, LPT-balanced request shards
         total_tokens = sum(s.total_tokens for s in specs)
         specs = [specs[i] for i in shard.lpt_shard([s.total_tokens for s in specs], world)[rank]]
@@ -609,8 +610,7 @@ def run_ours(args, rank, world, local_rank):
             "timing": "CUDA events on the launch stream around compress_batch, summed over steps",
         },
         "hbm_gbs_per_gpu": abytes * args.steps / (max_ms / 1e3) / 1e9,
-        "kept_tokens_per_s": (sum(compressed_spec(s, comp).total_tokens for s in specs) * world
-                              * args.steps / (max_ms / 1e3)),
+        "kept_tokens_per_s": job_kept * args.steps / (max_ms / 1e3),
         "roofline": {
             "bound": "hbm", "kernel": "press_kernel (score + top-k + in-place compaction)",
             "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
