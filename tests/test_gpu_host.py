@@ -78,6 +78,8 @@ CASES = [
      CompressorSpec(factor=4, press=PressKind.SNAPKV, window=32, pool_kernel=7), PoolMode.POOLED),
     ("float16", 1, 2, 2, 64, [(0, 300), (100, 21)],
      CompressorSpec(factor=4, press=PressKind.SNAPKV, window=16, pool_kernel=5), PoolMode.POOLED),
+    ("float16", 1, 2, 4, 128, [(576, 300), (0, 2600)],                  # tensor-core GQA + two-pass
+     CompressorSpec(factor=4, press=PressKind.SNAPKV, window=32, pool_kernel=7), PoolMode.POOLED),
     ("float16", 2, 2, 1, 128, [(576, 200), (0, 1024)],
      CompressorSpec(factor=4, press=PressKind.EXPECTED_ATTENTION, n_sink=4), PoolMode.POOLED),
     ("float16", 2, 2, 1, 128, [(48, 17), (0, 90)], CompressorSpec(factor=2, press=PressKind.KNORM),
@@ -110,7 +112,10 @@ def test_host_compress_equals_device_compress(cuda, dtype, L, H, gq, D, specs, c
     for i, (a, b) in enumerate(zip(dh, hh)):
         if ret:
             assert torch.equal(want.kept_idx[i], got.kept_idx[i]), i
-            assert np.array_equal(_bits(want.scores[i]), _bits(got.scores[i])), i
+            if gq == 1 or comp.press is not PressKind.SNAPKV:
+                assert np.array_equal(_bits(want.scores[i]), _bits(got.scores[i])), i
+            else:   # GQA SnapKV adds the heads' window means with float atomics (ulp-level order)
+                torch.testing.assert_close(got.scores[i], want.scores[i], rtol=1e-6, atol=0)
         assert np.array_equal(_bits(dev_pool.load_tokens(a)), _bits(host_pool.load_tokens(b))), i
         assert torch.equal(dev_pool._native.block_table_view(a.handle_id),
                            host_pool._native.block_table_view(b.handle_id))
