@@ -311,10 +311,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       float acc[16];
       // s1 = the window mean of both query groups (pass 3 adds into it)
       for (int t = ct - 8; t < T_len; t += kThreads) s1[t] = 0.f;
+      // GQA: each head's two group addends meet on a zeroed scratch (sc, unused until
+      // pooling) and are then added into s1 in head order -- deterministic
+      float* const wacc = kGqa ? sc : s1;
+      if (kGqa)
+        for (int t = ct; t < T_len; t += kThreads) sc[t] = 0.f;
       // GQA: one unit per query head of the group; each adds its window mean
-      // (weighted 1/(w * gq)) into s1 -- for gq = 1 the two groups' addends land
-      // on 0 (order-free), for gq > 1 the float atomics may differ in the last ulp
-      // from run to run
+      // (weighted 1/(w * gq)) into s1, in head order
       const int gq = kGqa ? pp.num_q_heads / g.H : 1;
       const float inv_wg = 1.0f / (float)(kWin * gq);
       for (int gi = 0; gi < gq; ++gi) {
@@ -410,7 +413,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             float sum = 0.f;
   #pragma unroll
             for (int j = 0; j < 16; ++j) sum = fmaf(v[j], zj[j], sum);   // masked entries are 0
-            atomicAdd(&s1[t], sum * inv_wg);
+            atomicAdd(&wacc[t], sum * inv_wg);   // two addends onto 0: order-free
           }
         }
         } else {
@@ -498,11 +501,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               float sum = 0.f;
   #pragma unroll
               for (int j = 0; j < 16; ++j) sum = fmaf(tc::ex2(fmaf(v[j], scale, -mj[j])), zj[j], sum);
-              atomicAdd(&s1[t], sum * inv_wg);
+              atomicAdd(&wacc[t], sum * inv_wg);   // two addends onto 0: order-free
             }
           }
         }
         gtile += ntiles > kSlots ? 2 * ntiles : ntiles;
+        if (kGqa) {
+          Consumers::sync();
+          for (int t = ct; t < T_len; t += kThreads) {
+            s1[t] += sc[t];
+            sc[t] = 0.f;
+          }
+        }
       }
       if (ct == 0) FC_STAMP(it, 4);
       Consumers::sync();
