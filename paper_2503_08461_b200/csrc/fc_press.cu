@@ -25,6 +25,10 @@
 
 #include "fc_select.cuh"
 
+#ifndef FC_KN_MINB  // Knorm CTAs per SM the register budget is sized for
+#define FC_KN_MINB 4
+#endif
+
 namespace fc {
 
 // ---------------------------------------------------------------------------
@@ -387,7 +391,7 @@ __host__ __device__ inline SmemPlan smem_plan(int kind, int max_T, int bs, int D
 }
 
 template <typename T, int D, int KIND>
-__global__ void __launch_bounds__(kThreads, KIND == FC_PRESS_KNORM ? 4 : 2)
+__global__ void __launch_bounds__(kThreads, KIND == FC_PRESS_KNORM ? FC_KN_MINB : 2)
     press_kernel(char* __restrict__ arena, const int32_t* __restrict__ src_table,
                  const int32_t* __restrict__ dst_table, const Geom g,
                  const __grid_constant__ PressBatch b, const PressParams pp,
