@@ -47,6 +47,8 @@ CONFIGS = {
            "tokens): segments beyond the 2048-token TMEM ring take the two-pass tensor-core path",
     "c3g": "SnapKV (window 32, pool 7) at 25% keep with GQA: Llama-3-8B-shaped KV (32 layers, 8 kv "
            "heads, 32 query heads, d=128), c3's 64 variable-length requests",
+    "c4g": "ExpectedAttention at 25% keep with GQA: Llama-3-8B-shaped KV (8 kv / 32 query heads), "
+           "c4w's 64 mixed-length requests (1k-8k tokens)",
     "c4w": "ExpectedAttention at 25% keep, 64 mixed-length requests (1k-8k tokens; one admission "
            "wave of config 4)",
     "c4": "ExpectedAttention at 25% keep on 256 mixed-length requests (1k-8k tokens) with pool "
@@ -61,8 +63,8 @@ CONFIGS = {
 }
 
 
-STRONG = {"c3", "c3g", "c3l", "c4w", "c4"}
-Q_HEADS = {"c3g": 32}   # query heads when they differ from the kv heads (GQA)
+STRONG = {"c3", "c3g", "c3l", "c4g", "c4w", "c4"}
+Q_HEADS = {"c3g": 32, "c4g": 32}   # query heads when they differ from the kv heads (GQA)
 
 
 def workload(name: str):
@@ -90,6 +92,12 @@ def workload(name: str):
         specs = [split_modalities(576, int(t)) for t in txt]
         return cfg, "float16", specs, CompressorSpec(factor=4, press=PressKind.SNAPKV, window=32,
                                                       pool_kernel=7)
+    if name == "c4g":
+        cfg = ModelConfig("llama-3-8b", 32, 8, 128, 2)
+        lens = np.random.default_rng(0).integers(1024, 8193, 256)[:64]
+        specs = [split_modalities(576, int(t) - 576) for t in lens]
+        return cfg, "float16", specs, CompressorSpec(factor=4, press=PressKind.EXPECTED_ATTENTION,
+                                                      n_sink=4)
     if name == "c3l":
         cfg = ModelConfig("llava-7b", 32, 32, 128, 2)
         lens = np.random.default_rng(0).integers(1024, 8193, 256)[:64]
@@ -202,8 +210,8 @@ def press_inputs(comp, cfg, n, device, torch, seed, hq=None):
         return {"q_window": q}
     if comp.press is PressKind.EXPECTED_ATTENTION:
         d = cfg.head_dim
-        mu = torch.randn((n, cfg.num_layers, cfg.num_kv_heads, d), generator=gen, device=device) / d ** 0.5
-        a = torch.randn((cfg.num_kv_heads, d, d), generator=gen, device=device)
+        mu = torch.randn((n, cfg.num_layers, hq, d), generator=gen, device=device) / d ** 0.5
+        a = torch.randn((hq, d, d), generator=gen, device=device)
         cov1 = a @ a.transpose(-1, -2) / d
         cov = cov1.expand(n, cfg.num_layers, -1, -1, -1).contiguous()
         return {"mean_q": mu.contiguous(), "cov_q": cov}

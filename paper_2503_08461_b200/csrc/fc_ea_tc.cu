@@ -84,17 +84,18 @@ struct Job {
 
 struct Smem {
   int max_nb, max_K;
-  int off_ring, off_b, off_zt, off_idx, off_ctab, off_bar, total;
+  int off_ring, off_b, off_zt, off_acc, off_idx, off_ctab, off_bar, total;
 };
 
-__host__ __device__ inline Smem plan(int bs, int max_T, int max_K) {
+__host__ __device__ inline Smem plan(int bs, int max_T, int max_K, bool gqa = false) {
   Smem p;
   p.max_nb = (max_T + bs - 1) / bs;
   p.max_K = max_K;
   p.off_ring = 0;
   p.off_b = p.off_ring + kStages * kStageBytes;
   p.off_zt = p.off_b + 2 * kBBytes;
-  p.off_idx = p.off_zt + ((max_T * 4 + 15) & ~15);
+  p.off_acc = p.off_zt + ((max_T * 4 + 15) & ~15);              // GQA: sum over heads of p_t
+  p.off_idx = p.off_acc + (gqa ? ((max_T * 4 + 15) & ~15) : 0);
   p.off_ctab = p.off_idx + 2 * ((max_K * 4 + 15) & ~15);
   p.off_bar = p.off_ctab + 2 * ((p.max_nb * 4 + 15) & ~15);
   p.total = p.off_bar + 64 * 8 + 1024;
@@ -110,13 +111,21 @@ __host__ __device__ inline Smem plan(int bs, int max_T, int max_K) {
 // K tile it waits on is exactly one phase ahead of its stage's last release.
 // (The old order [K][Sigma(next)][V] let the MMA reach the next K tile while
 // V stages were still in flight: a parity alias fed it a V tile, or hung it.)
+// GQA (gq query heads per kv head): one "unit" per head, each unit's K tiles
+// preceded by its own Sigma, so the sequence per segment is
+//   [K(u0)][Sigma(u1) x2][K(u1)] ... [K(u_last)][V tiles][Sigma(next seg, u0) x2]
+// and the MMA still only ever waits on K stages right after a Sigma it has
+// seen converted (b_full), which keeps the one-phase-ahead invariant.
 struct SegPos {
-  int k0, v0, sig_next, next;
+  int k0, v0, sig_next, next, unit_stride;
+  __device__ __forceinline__ int k_unit(int u) const { return k0 + u * unit_stride; }
+  __device__ __forceinline__ int sig_unit(int u) const { return k0 + (u - 1) * unit_stride + unit_stride - 2; }
 };
-__device__ __forceinline__ SegPos seg_pos(int start, int ntiles, bool has_next) {
+__device__ __forceinline__ SegPos seg_pos(int start, int ntiles, bool has_next, int gq = 1) {
   SegPos s;
   s.k0 = start;
-  s.v0 = start + ntiles;
+  s.unit_stride = ntiles + 2;                    // K tiles + the next unit's Sigma
+  s.v0 = start + gq * ntiles + 2 * (gq - 1);
   s.sig_next = s.v0 + ntiles;
   s.next = s.sig_next + (has_next ? 2 : 0);
   return s;
@@ -134,7 +143,7 @@ using namespace ea;
 
 // T = __half or __nv_bfloat16: the K/V tiles' type; Sigma / mu are split into
 // hi + lo parts of the same type (fp16: ~22 significant bits, bf16: ~16).
-template <typename T>
+template <typename T, bool kGqa>
 __global__ void __launch_bounds__(kEaThreads, 1)
     ea_tc_kernel(char* __restrict__ arena, const int32_t* __restrict__ table, const Geom g,
                  const __grid_constant__ PressBatch b, const PressParams pp,
@@ -149,10 +158,12 @@ __global__ void __launch_bounds__(kEaThreads, 1)
 
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  const Smem P = plan(g.bs, b.max_T, max_K);
+  const Smem P = plan(g.bs, b.max_T, max_K, kGqa);
+  const int gq = kGqa ? pp.num_q_heads / g.H : 1;
   unsigned char* ring = smem + P.off_ring;
   unsigned char* bmat = smem + P.off_b;  // [hi | lo]
   float* zt = reinterpret_cast<float*>(smem + P.off_zt);
+  float* pacc = reinterpret_cast<float*>(smem + P.off_acc);   // valid when kGqa
   const int k_stride = ((max_K * 4 + 15) & ~15) / 4;
   const int nb_stride = ((P.max_nb * 4 + 15) & ~15) / 4;
   int32_t* idxbuf = reinterpret_cast<int32_t*>(smem + P.off_idx);
@@ -216,10 +227,10 @@ __global__ void __launch_bounds__(kEaThreads, 1)
         __syncwarp();
         return ring + st * kStageBytes;
       };
-      auto load_sigma = [&](int item) {
+      auto load_sigma = [&](int item, int u) {
         const PressReq q = b.req[item / LH];
         const int lh = item % LH, l = lh / g.H, h = lh % g.H;
-        const int row = (int)((((int64_t)q.q_idx * g.L + l) * pp.num_q_heads + h) * kD);
+        const int row = (int)((((int64_t)q.q_idx * g.L + l) * pp.num_q_heads + h * gq + u) * kD);
         for (int part = 0; part < 2; ++part, ++pos) {
           unsigned char* dst = acquire(pos);
           uint64_t* bar = &st_full[pos % kStages];
@@ -247,13 +258,16 @@ __global__ void __launch_bounds__(kEaThreads, 1)
           }
         }
       };
-      if ((int)blockIdx.x < n_items) load_sigma(blockIdx.x);
+      if ((int)blockIdx.x < n_items) load_sigma(blockIdx.x, 0);
       for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         const int lh = item % LH, l = lh / g.H, h = lh % g.H;
         const PressReq q = b.req[item / LH];
-        load_tiles(q, l, h, 0);
+        for (int u = 0; u < gq; ++u) {
+          load_tiles(q, l, h, 0);                      // K tiles of unit u
+          if (u + 1 < gq) load_sigma(item, u + 1);
+        }
         load_tiles(q, l, h, 1);
-        if (item + (int)gridDim.x < n_items) load_sigma(item + gridDim.x);
+        if (item + (int)gridDim.x < n_items) load_sigma(item + gridDim.x, 0);
       }
     }
     __syncwarp();
@@ -262,15 +276,16 @@ __global__ void __launch_bounds__(kEaThreads, 1)
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_f16(Elem<T>::kDtype == FC_BF16 ? 1 : 0, kTileM, kBRows);
       const uint32_t bh = tc::smem_u32(bmat), bl = bh + kBBytes;
-      int pos = 2, gt = 0;
+      int pos = 2, gt = 0, un = 0;
       for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
         const PressReq q = b.req[item / LH];
         const int ntiles = (q.T + kTileM - 1) / kTileM;
-        const SegPos sp = seg_pos(pos, ntiles, item + (int)gridDim.x < n_items);
-        tc::mbar_wait(b_full, it & 1);
+        const SegPos sp = seg_pos(pos, ntiles, item + (int)gridDim.x < n_items, gq);
+        for (int u = 0; u < gq; ++u, ++un) {
+        tc::mbar_wait(b_full, un & 1);
         tc::fence_after_sync();
         for (int k = 0; k < ntiles; ++k, ++gt) {
-          const int p = sp.k0 + k, st = p % kStages, sl = gt % kSlots;
+          const int p = sp.k_unit(u) + k, st = p % kStages, sl = gt % kSlots;
           tc::mbar_wait(&sl_empty[sl], ((gt / kSlots) & 1) ^ 1);
           tc::mbar_wait(&st_full[st], (p / kStages) & 1);
           tc::fence_after_sync();
@@ -290,6 +305,7 @@ __global__ void __launch_bounds__(kEaThreads, 1)
           tc::mma_commit(&sl_full[sl]);
         }
         tc::mma_commit(b_empty);
+        }
         pos = sp.next;
       }
     }
@@ -330,10 +346,10 @@ __global__ void __launch_bounds__(kEaThreads, 1)
       if (lane == 0) tc::mbar_arrive(&st_empty[p % kStages]);
     };
     // Sigma (fp32, two ring stages) -> B hi/lo (fp16, transposed, swizzled) + mu row
-    auto convert_sigma = [&](int p0, int item) {
+    auto convert_sigma = [&](int p0, int item, int u) {
       const PressReq q = b.req[item / LH];
       const int lh = item % LH, l = lh / g.H, h = lh % g.H;
-      const float* mu = mean_q + ((((int64_t)q.q_idx * g.L + l) * pp.num_q_heads + h) * kD);
+      const float* mu = mean_q + ((((int64_t)q.q_idx * g.L + l) * pp.num_q_heads + h * gq + u) * kD);
       for (int part = 0; part < 2; ++part) {
         const int p = p0 + part;
         tc::mbar_wait(&st_full[p % kStages], (p / kStages) & 1);
@@ -365,25 +381,29 @@ __global__ void __launch_bounds__(kEaThreads, 1)
       if (ct == 0) tc::mbar_arrive(b_full);
     };
 
-    int pos = 2, gt = 0;
-    if ((int)blockIdx.x < n_items) convert_sigma(0, blockIdx.x);
+    int pos = 2, gt = 0, un = 0;
+    if ((int)blockIdx.x < n_items) convert_sigma(0, blockIdx.x, 0);
     for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
       const int r = item / LH, lh = item % LH, l = lh / g.H, h = lh % g.H;
       const PressReq q = b.req[r];
       const int T_len = q.T, K = q.K, ns = pp.n_sink;
       const int nb = (T_len + g.bs - 1) / g.bs, ntiles = (T_len + kTileM - 1) / kTileM;
       const bool has_next = item + (int)gridDim.x < n_items;
-      const SegPos sp = seg_pos(pos, ntiles, has_next);
+      const SegPos sp = seg_pos(pos, ntiles, has_next, gq);
       const int jb = it & 1;
-      for (int t = ct; t < T_len; t += kThreads) zt[t] = 0.f;
       if (ct == 0) {
         ss.first_drop = INT_MAX;
         EA_STAMP(it, 0);
       }
+      if (kGqa)
+        for (int t = ct; t < T_len; t += kThreads) pacc[t] = 0.f;
+      float m = -INFINITY, inv_z = 0.f;
+      for (int u = 0; u < gq; ++u, ++un) {
+      for (int t = ct; t < T_len; t += kThreads) zt[t] = 0.f;
       Consumers::sync();
       // ---- z_t from TMEM (Y = K.B^T) and the K rows still in SMEM ----
       for (int k = 0; k < ntiles; ++k, ++gt) {
-        const int p = sp.k0 + k, sl = gt % kSlots;
+        const int p = sp.k_unit(u) + k, sl = gt % kSlots;
         tc::mbar_wait(&sl_full[sl], (gt / kSlots) & 1);
         tc::fence_after_sync();
         float y[32];
@@ -420,7 +440,7 @@ __global__ void __launch_bounds__(kEaThreads, 1)
       Consumers::sync();
       if (ct == 0) EA_STAMP(it, 1);
       // ---- softmax over t >= n_sink ----
-      float m = -INFINITY;
+      m = -INFINITY;
       for (int t = ns + ct; t < T_len; t += kThreads) m = fmaxf(m, zt[t]);
 #pragma unroll
       for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
@@ -437,8 +457,19 @@ __global__ void __launch_bounds__(kEaThreads, 1)
       Consumers::sync();
       z = 0.f;
       for (int w = 0; w < kWarps; ++w) z += ss.red[w];
-      const float inv_z = 1.0f / z;
+      inv_z = 1.0f / z;
+      if (kGqa) {
+        // this head's probabilities join the running sum (heads in order: deterministic)
+        for (int t = ns + ct; t < T_len; t += kThreads) pacc[t] += expf(zt[t] - m) * inv_z;
+        if (u + 1 < gq) {                 // the next head's Sigma while the MMA idles
+          tc::mbar_wait(b_empty, un & 1);
+          convert_sigma(sp.sig_unit(u + 1), item, u + 1);
+        }
+      }
+      }
       if (ct == 0) EA_STAMP(it, 2);
+      if (kGqa) Consumers::sync();
+      const float inv_g = 1.0f / (float)gq;
       // ---- V tiles: s_t = p_t * ||V_t|| (two lanes per row) ----
       for (int k = 0; k < ntiles; ++k) {
         const int p = sp.v0 + k;
@@ -459,13 +490,14 @@ __global__ void __launch_bounds__(kEaThreads, 1)
         sq += __shfl_xor_sync(0xffffffffu, sq, 1);
         release_stage(p);
         const int t = k * kTileM + row;
-        if (half == 0 && t < T_len && t >= ns) zt[t] = expf(zt[t] - m) * inv_z * sqrtf(sq);
+        if (half == 0 && t < T_len && t >= ns)
+          zt[t] = (kGqa ? pacc[t] * inv_g : expf(zt[t] - m) * inv_z) * sqrtf(sq);
       }
       if (ct == 0) EA_STAMP(it, 3);
       // ---- the next segment's Sigma (last in the ring order, see SegPos) ----
       if (has_next) {
-        tc::mbar_wait(b_empty, it & 1);
-        convert_sigma(sp.sig_next, item + gridDim.x);
+        tc::mbar_wait(b_empty, (un - 1) & 1);   // the MMAs of this segment's last head
+        convert_sigma(sp.sig_next, item + gridDim.x, 0);
       }
       Consumers::sync();
       if (ct == 0) EA_STAMP(it, 4);
@@ -516,9 +548,9 @@ bool ea_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T,
   }();
   if (forced_simt) return false;
   if ((dtype != FC_F16 && dtype != FC_BF16) || g.D != kD) return false;
-  if (pp.num_q_heads != g.H) return false;   // one query head per kv head
+  if (pp.num_q_heads % g.H != 0 || pp.num_q_heads / g.H > 8) return false;   // GQA: gq <= 8
   if (g.bs < 8 || g.bs > 128) return false;
-  return plan(g.bs, max_T, max_K).total <= kDynSmemBudget;
+  return plan(g.bs, max_T, max_K, pp.num_q_heads != g.H).total <= kDynSmemBudget;
 }
 
 fc_status encode_rows(CUtensorMap* map, const void* base, int dtype, int D, uint64_t rows, int box_rows);
@@ -532,7 +564,8 @@ fc_status launch_ea_tc(const Geom& g, int dtype, char* arena, const int32_t* tab
   if (st != FC_OK) return st;
   st = encode_rows(&cmap, in.cov_q, FC_F32, g.D, (uint64_t)b.n_total * g.L * pp.num_q_heads * g.D, 64);
   if (st != FC_OK) return st;
-  const Smem P = plan(g.bs, b.max_T, max_K);
+  const bool gqa = pp.num_q_heads != g.H;
+  const Smem P = plan(g.bs, b.max_T, max_K, gqa);
   const int n_items = b.n * g.L * g.H;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -546,7 +579,9 @@ fc_status launch_ea_tc(const Geom& g, int dtype, char* arena, const int32_t* tab
     note_launch();
     return cuda_check(cudaGetLastError(), "ea_tc_kernel");
   };
-  return dtype == FC_BF16 ? launch(ea_tc_kernel<__nv_bfloat16>) : launch(ea_tc_kernel<__half>);
+  if (dtype == FC_BF16)
+    return gqa ? launch(ea_tc_kernel<__nv_bfloat16, true>) : launch(ea_tc_kernel<__nv_bfloat16, false>);
+  return gqa ? launch(ea_tc_kernel<__half, true>) : launch(ea_tc_kernel<__half, false>);
 }
 
 }  // namespace fc

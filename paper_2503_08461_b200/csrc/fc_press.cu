@@ -595,17 +595,38 @@ static fc_status launch_one(const Geom& g, char* arena, const int32_t* src, int3
     note_launch();
     return cuda_check(cudaGetLastError(), "chunk_pool_kernel");
   }
-  if (KIND == FC_PRESS_SNAPKV && b.in_place) {
+  if ((KIND == FC_PRESS_SNAPKV || KIND == FC_PRESS_EXPECTED_ATTENTION) && b.in_place) {
+    auto tc_ok = [&](int max_T, int max_K) {
+      return KIND == FC_PRESS_SNAPKV ? snapkv_tc_supported(g, Elem<T>::kDtype, pp, max_T, max_K)
+                                     : ea_tc_supported(g, Elem<T>::kDtype, pp, max_T, max_K);
+    };
+    auto run_tc = [&](const PressBatch& bb, int max_K) {
+      return KIND == FC_PRESS_SNAPKV
+                 ? launch_snapkv_tc(g, Elem<T>::kDtype, arena, src, bb, pp, in, out, stream)
+                 : launch_ea_tc(g, Elem<T>::kDtype, arena, src, bb, pp, in, out, max_K, stream);
+    };
     int max_K = 1;
     for (int i = 0; i < b.n; ++i) max_K = max_K > b.req[i].K ? max_K : b.req[i].K;
-    if (snapkv_tc_supported(g, Elem<T>::kDtype, pp, b.max_T, max_K))
-      return launch_snapkv_tc(g, Elem<T>::kDtype, arena, src, b, pp, in, out, stream);
-  }
-  if (KIND == FC_PRESS_EXPECTED_ATTENTION && b.in_place) {
-    int max_K = 1;
-    for (int i = 0; i < b.n; ++i) max_K = max_K > b.req[i].K ? max_K : b.req[i].K;
-    if (ea_tc_supported(g, Elem<T>::kDtype, pp, b.max_T, max_K))
-      return launch_ea_tc(g, Elem<T>::kDtype, arena, src, b, pp, in, out, max_K, stream);
+    if (tc_ok(b.max_T, max_K)) return run_tc(b, max_K);
+    // The tensor-core kernels size SMEM by the batch's longest request: when only
+    // some requests fit, split -- those go to the tensor-core kernel, the rest to
+    // the SIMT kernel (independent segments, so the split changes no result).
+    PressBatch fit = b, rest = b;
+    fit.n = rest.n = 0;
+    fit.max_T = rest.max_T = 0;
+    int fit_K = 1;
+    for (int i = 0; i < b.n; ++i) {
+      const PressReq& q = b.req[i];
+      PressBatch& dst = tc_ok(q.T, q.K > 0 ? q.K : 1) ? fit : rest;
+      dst.req[dst.n++] = q;
+      dst.max_T = std::max(dst.max_T, q.T);
+      if (&dst == &fit) fit_K = std::max(fit_K, q.K);
+    }
+    if (fit.n > 0 && rest.n > 0 && tc_ok(fit.max_T, fit_K)) {
+      fc_status st = run_tc(fit, fit_K);
+      if (st != FC_OK) return st;
+      return launch_one<T, D, KIND>(g, arena, src, dst, rest, pp, in, out, ws, ws_floats, stream);
+    }
   }
   const SmemPlan plan = smem_plan(KIND, b.max_T, g.bs, D, pp.window, b.in_place != 0, D * (int)sizeof(T));
   const int smem = plan.total();

@@ -165,3 +165,44 @@ def test_press_refusals_leave_the_batch_untouched(cuda):
     assert [h.spec.total_tokens for h in hs] == [8, 25]
     assert len(pool.ledger) == len(ledger) + 2
     pool.verify_conservation()
+
+
+@pytest.mark.parametrize("gq,specs", [
+    (1, [(0, 9000), (576, 500), (3, 1200)]),     # 9000 tokens exceed the EA tensor-core SMEM plan
+    (4, [(576, 6000), (0, 300), (17, 900)]),     # GQA: the per-head sum array leaves room for ~5k
+])
+def test_expected_attention_mixed_fit_batches(cuda, gq, specs):
+    """Requests that fit the tensor-core kernel run there, the rest on the SIMT kernel, in one
+    compress call; every score matches the oracle either way."""
+    cfg = ModelConfig("m", 1, 2, 128, 2)
+    pool = KVCachePool(cfg, (1 << 16) * cfg.bytes_per_token, device=cuda, kv_dtype="float16",
+                       max_handles=16, max_tokens_per_handle=16384, num_q_heads=2 * gq)
+    hs = pool.allocate_batch(list(range(len(specs))), [split_modalities(*s) for s in specs], 0.0)
+    pool.synth_fill(hs, seed=12)
+    raws = [_raw(pool, h, "float16") for h in hs]
+    gen = torch.Generator().manual_seed(5)
+    n, hq = len(specs), 2 * gq
+    mu = (torch.randn((n, 1, hq, 128), generator=gen) / 128 ** 0.5).float()
+    a = torch.randn((n, 1, hq, 128, 128), generator=gen)
+    cov = (a @ a.transpose(-1, -2) / 128).float().contiguous()
+    comp = CompressorSpec(factor=4, press=PressKind.EXPECTED_ATTENTION, n_sink=4)
+    res = pool.compress_batch(hs, comp, 1.0, mean_q=mu.to(cuda), cov_q=cov.to(cuda),
+                              return_indices=True, return_scores=True)
+    for i, s in enumerate(specs):
+        kv32 = osynth.to_f32(raws[i], "float16")
+        k_r = opress.kept_budget([x for x in s if x > 0], 4)
+        for h in range(2):
+            sl = slice(h * gq, (h + 1) * gq)
+            want = opress.expected_attention_scores(kv32[0, 0, h], kv32[0, 1, h], mu[i, 0, sl].numpy(),
+                                                    cov[i, 0, sl].numpy(), 4)
+            got = res.scores[i][0, h].cpu().numpy().astype(np.float64)
+            fin = np.isfinite(want)
+            assert np.array_equal(np.isfinite(got), fin)
+            rel = np.abs(got[fin] - want[fin]) / np.abs(want[fin])
+            assert rel.max() <= SCORE_RTOL, (i, h, rel.max())
+            kept = res.kept_idx[i][0, h].cpu().numpy()
+            assert opress.kept_set_mismatch(kept, want, k_r, SCORE_RTOL) is None
+        got_c = _raw(pool, hs[i], "float16")
+        assert np.array_equal(got_c.view(np.uint8),
+                              opress.gather_kept(raws[i], res.kept_idx[i].cpu().numpy()).view(np.uint8))
+    pool.verify_conservation()

@@ -256,6 +256,8 @@ def test_snapkv_parity(cuda, dtype, L, H, gq, D, specs, w, p):
     ("float16", 2, 2, 1, 128, [(576, 200), (0, 1024)], 4),               # tcgen05 path
     ("float16", 1, 2, 1, 128, [(576, 7616), (1, 1500), (0, 5), (130, 0)], 4),   # tcgen05, T=8192
     ("bfloat16", 2, 2, 1, 128, [(576, 200), (0, 1024), (576, 3000)], 4),     # tcgen05, bf16 hi/lo
+    ("float16", 2, 2, 2, 128, [(576, 200), (0, 1024), (3, 5)], 4),         # tcgen05 GQA g=2
+    ("bfloat16", 1, 2, 4, 128, [(576, 2000), (1, 300)], 4),                # tcgen05 GQA g=4
     ("bfloat16", 1, 2, 2, 64, [(0, 300)], 4),
     ("float32", 1, 1, 2, 128, [(30, 40)], 2),
 ])
