@@ -640,18 +640,27 @@ def run_ours(args, rank, world, local_rank):
     return result
 
 
+E2E_MAX_PINNED_BYTES = 64 * 10 ** 9
+
+
 def run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world, job_tokens):
     """Same metric through the public API with host buffers: every step hands the pool the
     batch's raw KV in pinned host memory (``compress_batch(host_kv=...)``) plus the press
     inputs (H2D), and reads the kept indices back (D2H)."""
     import torch
 
-    from paper_2503_08461_b200 import PoolMode, PressKind
+    from paper_2503_08461_b200 import PoolMode, PressKind, kv_bytes
 
     stream = torch.cuda.current_stream(device)
     n = len(specs)
     shapes = [(cfg.num_layers, 2, cfg.num_kv_heads, s.total_tokens, cfg.head_dim) for s in specs]
     tdt = getattr(torch, dtype)
+    host_bytes = sum(kv_bytes(cfg, s.total_tokens) for s in specs)
+    if host_bytes > E2E_MAX_PINNED_BYTES:
+        return {"value": None, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "skipped": f"the batch's raw KV ({host_bytes / 1e9:.0f} GB) exceeds the "
+                           f"{E2E_MAX_PINNED_BYTES / 1e9:.0f} GB of pinned host memory this "
+                           "measurement allocates"}
     hs = pool.allocate_batch(rids, specs, 0.0)
     pool.synth_fill(hs, seed=17)
     host = []
