@@ -567,9 +567,7 @@ fc_status launch_ea_tc(const Geom& g, int dtype, char* arena, const int32_t* tab
   const bool gqa = pp.num_q_heads != g.H;
   const Smem P = plan(g.bs, b.max_T, max_K, gqa);
   const int n_items = b.n * g.L * g.H;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count();
   const int grid = n_items < sms ? n_items : sms;
   auto launch = [&](auto kern) -> fc_status {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P.total);

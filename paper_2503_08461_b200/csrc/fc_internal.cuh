@@ -188,6 +188,9 @@ __device__ __forceinline__ uint32_t float_key(float f) {
 // ---------------------------------------------------------------------------
 // host-side launch helpers (defined in fc_pool.cu)
 // ---------------------------------------------------------------------------
+// SM count of the current device (queried once per device; 148 on B200): grids
+// are sized in multiples of it.
+int sm_count();
 void note_launch();
 fc_status set_error(fc_status st, const char* fmt, ...);
 fc_status cuda_check(cudaError_t e, const char* what);

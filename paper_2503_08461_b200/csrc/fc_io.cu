@@ -87,7 +87,7 @@ fc_status launch_synth(const Geom& g, int dtype, char* arena, const int32_t* tab
       max_vecs = vv > max_vecs ? vv : max_vecs;
     }
     int64_t gx = (max_vecs + 255) / 256;
-    const int64_t cap = (148LL * 8 * 4 + b.n - 1) / b.n;
+    const int64_t cap = ((int64_t)sm_count() * 8 * 4 + b.n - 1) / b.n;
     if (gx > cap) gx = cap;
     if (gx < 1) gx = 1;
     dim3 grid((unsigned)gx, (unsigned)b.n);
@@ -141,7 +141,7 @@ fc_status launch_store(const Geom& g, char* arena, const int32_t* table_row, int
   if (((uintptr_t)src) % 16) return set_error(FC_ERR_INVALID_ARG, "dense buffer must be 16-byte aligned");
   const int64_t total = (int64_t)g.L * nkv * g.H * n_tok * (g.row_bytes / 16);
   int64_t grid = (total + 255) / 256;
-  if (grid > 148 * 16) grid = 148 * 16;
+  if (grid > (int64_t)sm_count() * 16) grid = (int64_t)sm_count() * 16;
   store_tokens_kernel<<<(unsigned)grid, 256, 0, stream>>>(arena, table_row, g, tok_begin, n_tok,
                                                           (char*)src, to_blocks ? 1 : 0, kv0, nkv);
   note_launch();
@@ -208,7 +208,7 @@ fc_status launch_gather_host(const Geom& g, char* arena, const int32_t* table, i
       max_vecs = vv > max_vecs ? vv : max_vecs;
     }
     int64_t gx = (max_vecs + 1023) / 1024;
-    const int64_t cap = (148LL * 8 + b.n - 1) / b.n;
+    const int64_t cap = ((int64_t)sm_count() * 8 + b.n - 1) / b.n;
     if (gx > cap) gx = cap;
     if (gx < 1) gx = 1;
     gather_host_rows_kernel<<<dim3((unsigned)gx, (unsigned)b.n), 256, 0, stream>>>(arena, table, g, b,
@@ -288,7 +288,7 @@ fc_status launch_compress_tensor(const void* src, int64_t n, int64_t d, int dtyp
                                  const PressParams& pp, void* dst, cudaStream_t stream) {
   const int64_t rows = (n + pp.factor - 1) / pp.factor;
   int64_t grid = (rows * d + 255) / 256;
-  if (grid > 148 * 16) grid = 148 * 16;
+  if (grid > (int64_t)sm_count() * 16) grid = (int64_t)sm_count() * 16;
   if (grid < 1) grid = 1;
   switch (dtype) {
     case FC_F16:
@@ -378,7 +378,7 @@ fc_status launch_write_prefill(const Geom& g, char* arena, const int32_t* table,
 #define FC_PF_CTAS 64
 #endif
     int64_t gx = (max_vecs + 4095) / 4096;
-    const int64_t cap = (148LL * FC_PF_CTAS + b.n - 1) / b.n;
+    const int64_t cap = ((int64_t)sm_count() * FC_PF_CTAS + b.n - 1) / b.n;
     if (gx > cap) gx = cap;
     if (gx < 1) gx = 1;
     write_prefill_kernel<<<dim3((unsigned)gx, (unsigned)b.n), 256, 0, stream>>>(arena, table, g, b,

@@ -32,6 +32,20 @@ static thread_local int64_t g_launches = 0;
 
 void note_launch() { ++g_launches; }
 
+int sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      sms = 148;
+    cache[dev] = sms;
+  }
+  return cache[dev];
+}
+
 fc_status set_error(fc_status st, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
@@ -952,7 +966,7 @@ fc_status fc_pool_decode_attention(fc_pool* p, int32_t layer, int32_t n, const i
   // Split-KV only when (request, kv head) pairs alone cannot fill one wave of
   // 4 CTAs per SM: measured at c2d, 2-16 waves of splits cost 18-30% more
   // than the ragged 1.7-wave unsplit grid (partials + merge + short CTAs).
-  const int64_t want_items = 148 * 4;
+  const int64_t want_items = (int64_t)sm_count() * 4;
   int split = 1 << 30;
   if ((int64_t)n * p->g.H < want_items) {
     const int64_t s = (total_tok * p->g.H + want_items - 1) / want_items;

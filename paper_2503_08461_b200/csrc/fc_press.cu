@@ -573,9 +573,7 @@ int64_t press_workspace_floats(const Geom& g, int kind, int window, int num_q_he
   (void)g;
   (void)num_q_heads;
   if (kind != FC_PRESS_SNAPKV) return 0;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count();
   return (int64_t)sms * 4 * window * max_T;
 }
 
@@ -641,9 +639,7 @@ static fc_status launch_one(const Geom& g, char* arena, const int32_t* src, int3
   int64_t ws_per_cta = 0;
   if (KIND == FC_PRESS_SNAPKV) {
     ws_per_cta = (int64_t)pp.window * b.max_T;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = sm_count();
     grid = (int)std::min<int64_t>(n_items, std::min<int64_t>((int64_t)sms * 4, ws_floats / ws_per_cta));
   }
   kern<<<grid, kThreads, smem, stream>>>(arena, src, dst, g, b, pp, in, out, ws, ws_per_cta, n_items);

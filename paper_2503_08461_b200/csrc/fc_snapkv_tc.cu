@@ -650,9 +650,7 @@ fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t*
   for (int i = 0; i < b.n; ++i) max_K = max_K > b.req[i].K ? max_K : b.req[i].K;
   const TcSmem plan = tc_smem_plan(g.D, g.bs, b.max_T, max_K);
   const int n_items = b.n * g.L * g.H;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count();
   const int grid = n_items < sms ? n_items : sms;
   auto launch = [&](auto kern) -> fc_status {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.total);
