@@ -21,7 +21,10 @@
 
 namespace fc {
 
-constexpr int kDecodeWarps = 4;
+#ifndef FC_DEC_WARPS
+#define FC_DEC_WARPS 4
+#endif
+constexpr int kDecodeWarps = FC_DEC_WARPS;
 constexpr int kDecodeThreads = kDecodeWarps * 32;
 
 // The lane-group geometry of a row: kVpr 16-B vectors per row, kRows rows per
