@@ -53,7 +53,8 @@ __device__ __forceinline__ void ea_stamp(int it, int slot) {
 namespace ea {
 
 constexpr int kD = 128;
-constexpr int kStages = 3;
+constexpr int kStages = 3;                      // TMA ring depth (GQA: 2, see ea_stages)
+__host__ __device__ constexpr int ea_stages(bool gqa) { return gqa ? 2 : kStages; }
 constexpr int kTileM = 128;
 constexpr int kBRows = 144;                     // 128 Sigma^T rows + mu + 15 zero rows
 #ifndef FC_EA_CITEMS  // compactor 16-B loads in flight per thread per chunk
@@ -87,12 +88,14 @@ struct Smem {
   int off_ring, off_b, off_zt, off_acc, off_idx, off_ctab, off_bar, total;
 };
 
+// GQA gives one ring stage (32 KB) to the per-head probability sum so that
+// segments up to ~8k tokens still fit the 227-KB SMEM plan.
 __host__ __device__ inline Smem plan(int bs, int max_T, int max_K, bool gqa = false) {
   Smem p;
   p.max_nb = (max_T + bs - 1) / bs;
   p.max_K = max_K;
   p.off_ring = 0;
-  p.off_b = p.off_ring + kStages * kStageBytes;
+  p.off_b = p.off_ring + ea_stages(gqa) * kStageBytes;
   p.off_zt = p.off_b + 2 * kBBytes;
   p.off_acc = p.off_zt + ((max_T * 4 + 15) & ~15);              // GQA: sum over heads of p_t
   p.off_idx = p.off_acc + (gqa ? ((max_T * 4 + 15) & ~15) : 0);
@@ -158,6 +161,7 @@ __global__ void __launch_bounds__(kEaThreads, 1)
 
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int kStages = ea_stages(kGqa);
   const Smem P = plan(g.bs, b.max_T, max_K, kGqa);
   const int gq = kGqa ? pp.num_q_heads / g.H : 1;
   unsigned char* ring = smem + P.off_ring;
