@@ -148,7 +148,10 @@ __device__ void select_emit(const uint32_t* keys, int n, int K, int32_t* out, in
   const int need = exact ? 0 : krem;
   // Emission in super-tiles of kEmitR x 256 keys (warp w owns kEmitR x 32
   // consecutive keys, one ballot per 32): one barrier per super-tile.
-  constexpr int kEmitR = 4;
+#ifndef FC_EMIT_R
+#define FC_EMIT_R 4
+#endif
+  constexpr int kEmitR = FC_EMIT_R;
   int run_gt = 0, run_eq = 0, buf = 0;
   bool drop_found = false;
   for (int base = 0; base < n; base += kThreads * kEmitR, buf ^= 1) {
