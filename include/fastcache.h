@@ -245,6 +245,11 @@ FC_API fc_status fc_pool_set_profiling(fc_pool* pool, int32_t enable);
 /* Synchronising: timings of the most recent compress call. */
 FC_API fc_status fc_pool_last_profile(fc_pool* pool, fc_profile* out);
 
+/* Press launches of the most recent compress call per implementation:
+ * out[0] tensor-core (tcgen05/TMA/TMEM) kernels, out[1] SIMT press kernels,
+ * out[2] chunk-fold (MEAN_POOL / SEEDED_LINEAR) kernels. Not synchronising. */
+FC_API fc_status fc_pool_last_paths(fc_pool* pool, int64_t out[3]);
+
 /* Device pointer of a handle's block-table row and its live block count. */
 FC_API fc_status fc_pool_block_table(fc_pool* pool, int64_t handle_id, const int32_t** dev_row,
                               int32_t* n_blocks, int64_t* n_tokens);

@@ -44,6 +44,7 @@ EXPORTS = (
     "fc_pool_store_tokens", "fc_pool_load_tokens", "fc_synth_fill", "fc_compress_tensor",
     "fc_pool_set_profiling", "fc_pool_last_profile", "fc_pool_compress_host_batch",
     "fc_pool_write_kv", "fc_pool_decode_attention", "fc_pool_write_prefill_kv",
+    "fc_pool_last_paths",
 )
 
 
@@ -134,6 +135,7 @@ _SIGS = {
     "fc_compress_tensor": (_I32, [_P, _I64, _I64, _I32, ctypes.POINTER(PressConfigC), _P, _P]),
     "fc_pool_set_profiling": (_I32, [_P, _I32]),
     "fc_pool_last_profile": (_I32, [_P, ctypes.POINTER(ProfileC)]),
+    "fc_pool_last_paths": (_I32, [_P, _PI64]),
 }
 
 _lib = None

@@ -561,7 +561,7 @@ fc_status encode_rows(CUtensorMap* map, const void* base, int dtype, int D, uint
 
 fc_status launch_ea_tc(const Geom& g, int dtype, char* arena, const int32_t* table,
                        const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
-                       const fc_press_outputs& out, int max_K, cudaStream_t stream) {
+                       const fc_press_outputs& out, int max_K, cudaStream_t stream, bool dry_run) {
   CUtensorMap kmap, cmap;
   const uint64_t rows = (uint64_t)g.L * g.num_blocks * 2 * g.H * g.bs;
   fc_status st = encode_rows(&kmap, arena, dtype, g.D, rows, g.bs);
@@ -570,6 +570,9 @@ fc_status launch_ea_tc(const Geom& g, int dtype, char* arena, const int32_t* tab
   if (st != FC_OK) return st;
   const bool gqa = pp.num_q_heads != g.H;
   const Smem P = plan(g.bs, b.max_T, max_K, gqa);
+  if (P.total > kDynSmemBudget)
+    return set_error(FC_ERR_UNSUPPORTED, "ExpectedAttention tensor-core plan exceeds the SMEM budget");
+  if (dry_run) return FC_OK;
   const int n_items = b.n * g.L * g.H;
   const int sms = sm_count();
   const int grid = n_items < sms ? n_items : sms;
@@ -579,6 +582,7 @@ fc_status launch_ea_tc(const Geom& g, int dtype, char* arena, const int32_t* tab
     kern<<<grid, kEaThreads, P.total, stream>>>(arena, table, g, b, pp, kmap, cmap, in.mean_q, out,
                                                 n_items, max_K);
     note_launch();
+    note_path(kPathTc);
     return cuda_check(cudaGetLastError(), "ea_tc_kernel");
   };
   if (dtype == FC_BF16)

@@ -192,6 +192,11 @@ __device__ __forceinline__ uint32_t float_key(float f) {
 // are sized in multiples of it.
 int sm_count();
 void note_launch();
+// Which press implementation a launch used (tensor-core, SIMT, chunk fold): counted
+// per thread so a compress call can report the path it took (fc_pool_last_paths).
+enum PressPath { kPathTc = 0, kPathSimt = 1, kPathChunk = 2, kNumPaths = 3 };
+void note_path(int path);
+int64_t path_count(int path);
 fc_status set_error(fc_status st, const char* fmt, ...);
 fc_status cuda_check(cudaError_t e, const char* what);
 
@@ -199,15 +204,16 @@ fc_status cuda_check(cudaError_t e, const char* what);
 fc_status launch_press(const Geom& g, int dtype, char* arena, const int32_t* src_table,
                        int32_t* dst_table, const PressBatch& batch, const PressParams& pp,
                        const fc_press_inputs* in, const fc_press_outputs* out, float* workspace,
-                       int64_t workspace_floats, int32_t* d_err, cudaStream_t stream);
+                       int64_t workspace_floats, int32_t* d_err, cudaStream_t stream,
+                       bool dry_run = false);
 bool snapkv_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T, int max_K);
 fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t* table,
                            const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
-                           const fc_press_outputs& out, cudaStream_t stream);
+                           const fc_press_outputs& out, cudaStream_t stream, bool dry_run);
 bool ea_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T, int max_K);
 fc_status launch_ea_tc(const Geom& g, int dtype, char* arena, const int32_t* table,
                        const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
-                       const fc_press_outputs& out, int max_K, cudaStream_t stream);
+                       const fc_press_outputs& out, int max_K, cudaStream_t stream, bool dry_run);
 int64_t press_workspace_floats(const Geom& g, int kind, int window, int num_q_heads, int max_T);
 
 // decode kernels (fc_decode.cu)

@@ -29,8 +29,11 @@ namespace fc {
 
 static thread_local char g_err[512] = "";
 static thread_local int64_t g_launches = 0;
+static thread_local int64_t g_paths[kNumPaths] = {0, 0, 0};
 
 void note_launch() { ++g_launches; }
+void note_path(int path) { ++g_paths[path]; }
+int64_t path_count(int path) { return g_paths[path]; }
 
 int sm_count() {
   static int cache[64] = {0};
@@ -151,6 +154,7 @@ struct fc_pool {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, press_end, free_end, end
   int64_t prof_press_launches = 0, prof_total_launches = 0;
   bool prof_valid = false;
+  int64_t last_paths[kNumPaths] = {0, 0, 0};  // press launches per path, last compress call
   // host-resident compress (fc_pool_compress_host_batch): a copy stream, two
   // staging slots the DMA fills while the previous slot is scattered into
   // blocks, and a kept-index scratch for the zero-copy V gather.
@@ -283,6 +287,9 @@ fc_status fc_pool_create(const fc_model_config* cfg, uint64_t capacity_bytes,
   if (capacity_bytes < 1) return set_error(FC_ERR_INVALID_ARG, "capacity_bytes must be >= 1");
   if (opts->block_size < 1 || opts->max_handles < 1 || opts->max_blocks_per_handle < 1)
     return set_error(FC_ERR_INVALID_ARG, "block_size, max_handles, max_blocks_per_handle must be >= 1");
+  if (cfg->dtype == FC_U8)
+    return set_error(FC_ERR_UNSUPPORTED,
+                     "device pools need a float KV dtype (f16/bf16/f32): the presses score K");
   if (opts->block_size & (opts->block_size - 1))
     return set_error(FC_ERR_UNSUPPORTED, "block_size must be a power of two");
   if (((int64_t)cfg->head_dim * cfg->bytes_per_element) % 16 != 0)
@@ -307,7 +314,8 @@ fc_status fc_pool_create(const fc_model_config* cfg, uint64_t capacity_bytes,
   g.max_bpr = opts->max_blocks_per_handle;
   g.num_blocks = opts->num_blocks > 0
                      ? opts->num_blocks
-                     : (int64_t)(capacity_bytes / p->block_bytes) + opts->max_handles;
+                     : (int64_t)(capacity_bytes / p->block_bytes) +
+                           (int64_t)opts->max_handles * (opts->mode == FC_LEGACY_ZOMBIE ? 2 : 1);
   if (g.num_blocks > INT32_MAX) {
     delete p;
     return set_error(FC_ERR_INVALID_ARG, "num_blocks exceeds int32 block ids");
@@ -525,21 +533,8 @@ fc_status fc_pool_compress_batch(fc_pool* p, int32_t n, const int64_t* handle_id
   const int bs = p->g.bs;
 
   DeviceGuard guard(p->device);
-  const int64_t launches0 = g_launches;
-  if (p->profiling) cudaEventRecord(p->ev[0], stream);
-  // Legacy: move the raw rows aside and pop fresh destination blocks (batch order).
-  if (legacy) {
-    std::vector<BlockOp> ops(n);
-    std::vector<int32_t> save(n);
-    for (int i = 0; i < n; ++i) {
-      ops[i] = BlockOp{slot[i], 0, (int32_t)blocks_for(kept[i], bs), 0};
-      save[i] = p->slots[slot[i]].n_blocks;
-    }
-    st = run_block_ops(p, ops, true, true, save, stream);
-    if (st != FC_OK) return st;
-  }
-
-  // Host-side weight table for SEEDEDLINEAR (row m-1 = renormalised w[:m]).
+  // Plan every launch chunk first: offsets in batch order, launch order LPT
+  // (longest request first), chunks of kMaxBatch requests.
   PressParams pp{};
   pp.kind = press->kind;
   pp.factor = press->factor;
@@ -548,20 +543,6 @@ fc_status fc_pool_compress_batch(fc_pool* p, int32_t n, const int64_t* handle_id
   pp.n_sink = press->n_sink;
   pp.num_q_heads = press->num_q_heads;
   pp.w_table = p->d_wtable;
-  if (press->kind == FC_PRESS_SEEDEDLINEAR) {
-    std::vector<double> wt((size_t)press->factor * press->factor, 0.0);
-    for (int m = 1; m <= press->factor; ++m) {
-      double s = 0;
-      for (int i = 0; i < m; ++i) s += press->chunk_weights[i];
-      for (int i = 0; i < m; ++i) wt[(size_t)(m - 1) * press->factor + i] = press->chunk_weights[i] / s;
-    }
-    st = cuda_check(cudaMemcpyAsync(p->d_wtable, wt.data(), wt.size() * sizeof(double),
-                                    cudaMemcpyHostToDevice, stream),
-                    "upload chunk weights");
-    if (st != FC_OK) return st;
-  }
-
-  // Output offsets in batch order; launch order LPT (longest request first).
   std::vector<int64_t> kept_off(n), score_off(n);
   int64_t ko = 0, so = 0;
   const int64_t LH = (int64_t)p->g.L * p->g.H;
@@ -576,8 +557,11 @@ fc_status fc_pool_compress_batch(fc_pool* p, int32_t n, const int64_t* handle_id
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
     return p->slots[slot[a]].tokens > p->slots[slot[b]].tokens;
   });
+  std::vector<PressBatch> chunks;
+  int64_t need_ws = 0;
   for (int c = 0; c < n; c += kMaxBatch) {
-    PressBatch b;
+    chunks.emplace_back();
+    PressBatch& b = chunks.back();
     memset(&b, 0, sizeof(b));
     b.n = std::min(kMaxBatch, n - c);
     b.per_segment = press->kind <= FC_PRESS_EXPECTED_ATTENTION ? 0 : 1;
@@ -598,19 +582,63 @@ fc_status fc_pool_compress_batch(fc_pool* p, int32_t n, const int64_t* handle_id
       b.max_T = std::max<int32_t>(b.max_T, q.T);
     }
     if (press->per_segment) b.per_segment = 1;
-    const int64_t need_ws =
-        press_workspace_floats(p->g, press->kind, press->window, press->num_q_heads, b.max_T);
-    if (need_ws > p->ws_floats) {
-      cudaFree(p->d_ws);
-      p->d_ws = nullptr;
-      st = cuda_check(cudaMalloc(&p->d_ws, need_ws * sizeof(float)), "cudaMalloc(workspace)");
-      if (st != FC_OK) return st;
-      p->ws_floats = need_ws;
-    }
-    st = launch_press(p->g, p->cfg.dtype, p->arena, legacy ? p->d_rtable : p->d_table, p->d_table,
-                      b, pp, inputs, outputs, p->d_ws, p->ws_floats, p->d_err, stream);
+    need_ws = std::max(need_ws, press_workspace_floats(p->g, press->kind, press->window,
+                                                       press->num_q_heads, b.max_T));
+  }
+  // Dry-run every chunk's launch plan (dtype, head_dim, SMEM budget, tensor-core /
+  // SIMT split, tensor maps) and size the workspace BEFORE any pop, push or
+  // launch: a refused batch leaves blocks, tables, payload and ledger untouched
+  // (the reference's all-or-nothing mutations, pool.py:147-165,167-192).
+  const int32_t* src_table = legacy ? p->d_rtable : p->d_table;
+  for (const PressBatch& b : chunks) {
+    st = launch_press(p->g, p->cfg.dtype, p->arena, src_table, p->d_table, b, pp, inputs, outputs,
+                      p->d_ws, p->ws_floats, p->d_err, stream, /*dry_run=*/true);
     if (st != FC_OK) return st;
   }
+  if (need_ws > p->ws_floats) {
+    cudaStreamSynchronize(stream);
+    cudaFree(p->d_ws);
+    p->d_ws = nullptr;
+    p->ws_floats = 0;
+    st = cuda_check(cudaMalloc(&p->d_ws, need_ws * sizeof(float)), "cudaMalloc(workspace)");
+    if (st != FC_OK) return st;
+    p->ws_floats = need_ws;
+  }
+  // Host-side weight table for SEEDEDLINEAR (row m-1 = renormalised w[:m]).
+  if (press->kind == FC_PRESS_SEEDEDLINEAR) {
+    std::vector<double> wt((size_t)press->factor * press->factor, 0.0);
+    for (int m = 1; m <= press->factor; ++m) {
+      double s = 0;
+      for (int i = 0; i < m; ++i) s += press->chunk_weights[i];
+      for (int i = 0; i < m; ++i) wt[(size_t)(m - 1) * press->factor + i] = press->chunk_weights[i] / s;
+    }
+    st = cuda_check(cudaMemcpyAsync(p->d_wtable, wt.data(), wt.size() * sizeof(double),
+                                    cudaMemcpyHostToDevice, stream),
+                    "upload chunk weights");
+    if (st != FC_OK) return st;
+  }
+
+  const int64_t launches0 = g_launches;
+  int64_t paths0[kNumPaths];
+  for (int k = 0; k < kNumPaths; ++k) paths0[k] = path_count(k);
+  if (p->profiling) cudaEventRecord(p->ev[0], stream);
+  // Legacy: move the raw rows aside and pop fresh destination blocks (batch order).
+  if (legacy) {
+    std::vector<BlockOp> ops(n);
+    std::vector<int32_t> save(n);
+    for (int i = 0; i < n; ++i) {
+      ops[i] = BlockOp{slot[i], 0, (int32_t)blocks_for(kept[i], bs), 0};
+      save[i] = p->slots[slot[i]].n_blocks;
+    }
+    st = run_block_ops(p, ops, true, true, save, stream);
+    if (st != FC_OK) return st;
+  }
+  for (const PressBatch& b : chunks) {
+    st = launch_press(p->g, p->cfg.dtype, p->arena, src_table, p->d_table, b, pp, inputs, outputs,
+                      p->d_ws, p->ws_floats, p->d_err, stream);
+    if (st != FC_OK) return st;
+  }
+  for (int k = 0; k < kNumPaths; ++k) p->last_paths[k] = path_count(k) - paths0[k];
 
   int64_t press_launches = g_launches - launches0;
   if (p->profiling) cudaEventRecord(p->ev[1], stream);
@@ -748,8 +776,6 @@ fc_status fc_pool_compress_host_batch(fc_pool* p, int32_t n, const int64_t* hand
     if (sum_kept > p->kept_cap) {
       cudaStreamSynchronize(stream);
       cudaFree(p->d_kept);
-  cudaFree(p->d_dec_ws);
-  cudaFree(p->d_dec_ctr);
       p->d_kept = nullptr;
       p->kept_cap = 0;
       st = cuda_check(cudaMalloc(&p->d_kept, sum_kept * sizeof(int32_t)), "cudaMalloc(kept)");
@@ -777,7 +803,13 @@ fc_status fc_pool_append(fc_pool* p, int32_t n, const int64_t* handle_ids, const
                          uint64_t* requested_out, uint64_t* available_out, void* stream) {
   if (!p || n < 0 || (n > 0 && (!handle_ids || !tokens)))
     return set_error(FC_ERR_INVALID_ARG, "bad arguments");
+  // Validate the whole batch -- bytes, per-handle block rows AND the block demand
+  // on the free stack -- before mutating anything (pool.py:194-211 is strict and
+  // all-or-nothing). Members may repeat a handle: each sees its predecessors' growth.
   std::vector<int32_t> slot(n);
+  std::vector<int64_t> new_tokens(n);
+  std::vector<BlockOp> ops;
+  std::unordered_map<int32_t, std::pair<int64_t, int32_t>> grown;  // slot -> (tokens, blocks)
   uint64_t cur = p->current;
   int64_t blocks = 0;
   for (int i = 0; i < n; ++i) {
@@ -796,30 +828,33 @@ fc_status fc_pool_append(fc_pool* p, int32_t n, const int64_t* handle_ids, const
                        (unsigned long long)need, (unsigned long long)(p->capacity - cur));
     }
     cur += need;
-    int64_t total = sl.tokens + tokens[i];
-    for (int j = 0; j < i; ++j)
-      if (slot[j] == slot[i]) total += tokens[j];
-    if (blocks_for(total, p->g.bs) > p->g.max_bpr)
-      return set_error(FC_ERR_INVALID_ARG, "handle exceeds max_blocks_per_handle");
+    auto it = grown.find(slot[i]);
+    const int64_t t0 = it == grown.end() ? sl.tokens : it->second.first;
+    const int32_t b0 = it == grown.end() ? sl.n_blocks : it->second.second;
+    const int64_t t1 = t0 + tokens[i];
+    const int64_t b1 = blocks_for(t1, p->g.bs);
+    if (b1 > p->g.max_bpr) return set_error(FC_ERR_INVALID_ARG, "handle exceeds max_blocks_per_handle");
+    if (b1 > b0) {
+      blocks += b1 - b0;
+      ops.push_back(BlockOp{slot[i], b0, (int32_t)(b1 - b0), 0});
+    }
+    grown[slot[i]] = {t1, (int32_t)std::max<int64_t>(b0, b1)};
+    new_tokens[i] = t1;
   }
+  if (blocks > p->top) return set_error(FC_ERR_CAPACITY, "block pool exhausted");
   DeviceGuard guard(p->device);
-  std::vector<BlockOp> ops;
+  fc_status st = run_block_ops(p, ops, true, false, {}, (cudaStream_t)stream);
+  if (st != FC_OK) return st;
   for (int i = 0; i < n; ++i) {
     Slot& sl = p->slots[slot[i]];
-    const int32_t nb = (int32_t)blocks_for(sl.tokens + tokens[i], p->g.bs);
-    if (nb > sl.n_blocks) {
-      blocks += nb - sl.n_blocks;
-      ops.push_back(BlockOp{slot[i], sl.n_blocks, nb - sl.n_blocks, 0});
-    }
     uint64_t need;
     tok_bytes(p, tokens[i], &need);
-    sl.tokens += tokens[i];
-    sl.n_blocks = nb;
+    sl.tokens = new_tokens[i];
+    sl.n_blocks = (int32_t)blocks_for(sl.tokens, p->g.bs);
     sl.bytes += need;
     apply(p, (int64_t)need);
   }
-  if (blocks > p->top) return set_error(FC_ERR_CAPACITY, "block pool exhausted");
-  return run_block_ops(p, ops, true, false, {}, (cudaStream_t)stream);
+  return FC_OK;
 }
 
 fc_status fc_pool_release_batch(fc_pool* p, int32_t n, const int64_t* handle_ids, void* stream) {
@@ -1081,6 +1116,12 @@ fc_status fc_pool_last_profile(fc_pool* p, fc_profile* out) {
   out->total_ms = c;
   out->press_launches = p->prof_press_launches;
   out->total_launches = p->prof_total_launches;
+  return FC_OK;
+}
+
+fc_status fc_pool_last_paths(fc_pool* p, int64_t out[3]) {
+  if (!p || !out) return set_error(FC_ERR_INVALID_ARG, "null argument");
+  for (int k = 0; k < kNumPaths; ++k) out[k] = p->last_paths[k];
   return FC_OK;
 }
 

@@ -581,16 +581,20 @@ template <typename T, int D, int KIND>
 static fc_status launch_one(const Geom& g, char* arena, const int32_t* src, int32_t* dst,
                             const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
                             const fc_press_outputs& out, float* ws, int64_t ws_floats,
-                            cudaStream_t stream) {
+                            cudaStream_t stream, bool dry) {
   const int n_items = b.n * g.L * g.H;
   if (KIND == FC_PRESS_MEANPOOL || KIND == FC_PRESS_SEEDEDLINEAR) {
     const int nb = (b.max_T + g.bs - 1) / g.bs;
     const int smem = align16(nb * 4) * 2;
+    if (smem > kDynSmemBudget)
+      return set_error(FC_ERR_UNSUPPORTED, "request of %d tokens exceeds the chunk-fold SMEM plan", b.max_T);
+    if (dry) return FC_OK;
     auto kern = chunk_pool_kernel<T, D>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<n_items, kThreads, smem, stream>>>(arena, src, dst, g, b, pp);
     note_launch();
+    note_path(kPathChunk);
     return cuda_check(cudaGetLastError(), "chunk_pool_kernel");
   }
   if ((KIND == FC_PRESS_SNAPKV || KIND == FC_PRESS_EXPECTED_ATTENTION) && b.in_place) {
@@ -600,8 +604,8 @@ static fc_status launch_one(const Geom& g, char* arena, const int32_t* src, int3
     };
     auto run_tc = [&](const PressBatch& bb, int max_K) {
       return KIND == FC_PRESS_SNAPKV
-                 ? launch_snapkv_tc(g, Elem<T>::kDtype, arena, src, bb, pp, in, out, stream)
-                 : launch_ea_tc(g, Elem<T>::kDtype, arena, src, bb, pp, in, out, max_K, stream);
+                 ? launch_snapkv_tc(g, Elem<T>::kDtype, arena, src, bb, pp, in, out, stream, dry)
+                 : launch_ea_tc(g, Elem<T>::kDtype, arena, src, bb, pp, in, out, max_K, stream, dry);
     };
     int max_K = 1;
     for (int i = 0; i < b.n; ++i) max_K = max_K > b.req[i].K ? max_K : b.req[i].K;
@@ -623,13 +627,14 @@ static fc_status launch_one(const Geom& g, char* arena, const int32_t* src, int3
     if (fit.n > 0 && rest.n > 0 && tc_ok(fit.max_T, fit_K)) {
       fc_status st = run_tc(fit, fit_K);
       if (st != FC_OK) return st;
-      return launch_one<T, D, KIND>(g, arena, src, dst, rest, pp, in, out, ws, ws_floats, stream);
+      return launch_one<T, D, KIND>(g, arena, src, dst, rest, pp, in, out, ws, ws_floats, stream, dry);
     }
   }
   const SmemPlan plan = smem_plan(KIND, b.max_T, g.bs, D, pp.window, b.in_place != 0, D * (int)sizeof(T));
   const int smem = plan.total();
   if (smem > 220 * 1024)
     return set_error(FC_ERR_UNSUPPORTED, "request of %d tokens exceeds the SMEM budget", b.max_T);
+  if (dry) return FC_OK;
   auto kern = press_kernel<T, D, KIND == FC_PRESS_KNORM ? FC_PRESS_KNORM
                                    : KIND == FC_PRESS_SNAPKV ? FC_PRESS_SNAPKV
                                                              : FC_PRESS_EXPECTED_ATTENTION>;
@@ -644,6 +649,7 @@ static fc_status launch_one(const Geom& g, char* arena, const int32_t* src, int3
   }
   kern<<<grid, kThreads, smem, stream>>>(arena, src, dst, g, b, pp, in, out, ws, ws_per_cta, n_items);
   note_launch();
+  note_path(kPathSimt);
   return cuda_check(cudaGetLastError(), "press_kernel");
 }
 
@@ -651,16 +657,16 @@ template <typename T, int D>
 static fc_status dispatch_kind(int kind, const Geom& g, char* arena, const int32_t* src,
                                int32_t* dst, const PressBatch& b, const PressParams& pp,
                                const fc_press_inputs& in, const fc_press_outputs& out, float* ws,
-                               int64_t wsf, cudaStream_t s) {
+                               int64_t wsf, cudaStream_t s, bool dry) {
   switch (kind) {
     case FC_PRESS_KNORM:
-      return launch_one<T, D, FC_PRESS_KNORM>(g, arena, src, dst, b, pp, in, out, ws, wsf, s);
+      return launch_one<T, D, FC_PRESS_KNORM>(g, arena, src, dst, b, pp, in, out, ws, wsf, s, dry);
     case FC_PRESS_SNAPKV:
-      return launch_one<T, D, FC_PRESS_SNAPKV>(g, arena, src, dst, b, pp, in, out, ws, wsf, s);
+      return launch_one<T, D, FC_PRESS_SNAPKV>(g, arena, src, dst, b, pp, in, out, ws, wsf, s, dry);
     case FC_PRESS_EXPECTED_ATTENTION:
-      return launch_one<T, D, FC_PRESS_EXPECTED_ATTENTION>(g, arena, src, dst, b, pp, in, out, ws, wsf, s);
+      return launch_one<T, D, FC_PRESS_EXPECTED_ATTENTION>(g, arena, src, dst, b, pp, in, out, ws, wsf, s, dry);
     default:
-      return launch_one<T, D, FC_PRESS_MEANPOOL>(g, arena, src, dst, b, pp, in, out, ws, wsf, s);
+      return launch_one<T, D, FC_PRESS_MEANPOOL>(g, arena, src, dst, b, pp, in, out, ws, wsf, s, dry);
   }
 }
 
@@ -668,11 +674,11 @@ template <typename T>
 static fc_status dispatch_dim(int kind, const Geom& g, char* arena, const int32_t* src,
                               int32_t* dst, const PressBatch& b, const PressParams& pp,
                               const fc_press_inputs& in, const fc_press_outputs& out, float* ws,
-                              int64_t wsf, cudaStream_t s) {
+                              int64_t wsf, cudaStream_t s, bool dry) {
   switch (g.D) {
-    case 64: return dispatch_kind<T, 64>(kind, g, arena, src, dst, b, pp, in, out, ws, wsf, s);
-    case 128: return dispatch_kind<T, 128>(kind, g, arena, src, dst, b, pp, in, out, ws, wsf, s);
-    case 256: return dispatch_kind<T, 256>(kind, g, arena, src, dst, b, pp, in, out, ws, wsf, s);
+    case 64: return dispatch_kind<T, 64>(kind, g, arena, src, dst, b, pp, in, out, ws, wsf, s, dry);
+    case 128: return dispatch_kind<T, 128>(kind, g, arena, src, dst, b, pp, in, out, ws, wsf, s, dry);
+    case 256: return dispatch_kind<T, 256>(kind, g, arena, src, dst, b, pp, in, out, ws, wsf, s, dry);
     default: return set_error(FC_ERR_UNSUPPORTED, "head_dim %d has no compiled press kernel", g.D);
   }
 }
@@ -680,7 +686,7 @@ static fc_status dispatch_dim(int kind, const Geom& g, char* arena, const int32_
 fc_status launch_press(const Geom& g, int dtype, char* arena, const int32_t* src_table,
                        int32_t* dst_table, const PressBatch& batch, const PressParams& pp,
                        const fc_press_inputs* in_p, const fc_press_outputs* out_p, float* ws,
-                       int64_t ws_floats, int32_t* d_err, cudaStream_t stream) {
+                       int64_t ws_floats, int32_t* d_err, cudaStream_t stream, bool dry) {
   (void)d_err;
   fc_press_inputs in{};
   fc_press_outputs out{};
@@ -688,11 +694,11 @@ fc_status launch_press(const Geom& g, int dtype, char* arena, const int32_t* src
   if (out_p) out = *out_p;
   switch (dtype) {
     case FC_F16:
-      return dispatch_dim<__half>(pp.kind, g, arena, src_table, dst_table, batch, pp, in, out, ws, ws_floats, stream);
+      return dispatch_dim<__half>(pp.kind, g, arena, src_table, dst_table, batch, pp, in, out, ws, ws_floats, stream, dry);
     case FC_BF16:
-      return dispatch_dim<__nv_bfloat16>(pp.kind, g, arena, src_table, dst_table, batch, pp, in, out, ws, ws_floats, stream);
+      return dispatch_dim<__nv_bfloat16>(pp.kind, g, arena, src_table, dst_table, batch, pp, in, out, ws, ws_floats, stream, dry);
     case FC_F32:
-      return dispatch_dim<float>(pp.kind, g, arena, src_table, dst_table, batch, pp, in, out, ws, ws_floats, stream);
+      return dispatch_dim<float>(pp.kind, g, arena, src_table, dst_table, batch, pp, in, out, ws, ws_floats, stream, dry);
     default:
       return set_error(FC_ERR_UNSUPPORTED, "press kernels need an f16/bf16/f32 pool");
   }

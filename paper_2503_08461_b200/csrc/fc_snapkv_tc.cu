@@ -637,7 +637,7 @@ bool snapkv_tc_supported(const Geom& g, int dtype, const PressParams& pp, int ma
 
 fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t* table,
                            const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
-                           const fc_press_outputs& out, cudaStream_t stream) {
+                           const fc_press_outputs& out, cudaStream_t stream, bool dry_run) {
   const int n_requests_total = b.n_total;
   CUtensorMap kmap, qmap;
   const uint64_t rows = (uint64_t)g.L * g.num_blocks * 2 * g.H * g.bs;
@@ -649,6 +649,9 @@ fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t*
   int max_K = 1;
   for (int i = 0; i < b.n; ++i) max_K = max_K > b.req[i].K ? max_K : b.req[i].K;
   const TcSmem plan = tc_smem_plan(g.D, g.bs, b.max_T, max_K);
+  if (plan.total > kDynSmemBudget)
+    return set_error(FC_ERR_UNSUPPORTED, "SnapKV tensor-core plan exceeds the SMEM budget");
+  if (dry_run) return FC_OK;
   const int n_items = b.n * g.L * g.H;
   const int sms = sm_count();
   const int grid = n_items < sms ? n_items : sms;
@@ -658,6 +661,7 @@ fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t*
     kern<<<grid, kTcThreads, plan.total, stream>>>(arena, table, g, b, pp, kmap, qmap, out, n_items,
                                                    max_K);
     note_launch();
+    note_path(kPathTc);
     return cuda_check(cudaGetLastError(), "snapkv_tc_kernel");
   };
   // g = 1 gets its own instantiation (the unit loop folds away)

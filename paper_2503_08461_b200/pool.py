@@ -192,6 +192,11 @@ class _NativePool:
             self.device = torch.device("cuda", torch.cuda.current_device())
         if kv_dtype not in _TORCH_DTYPES:
             raise ValueError(f"kv_dtype must be one of {sorted(_TORCH_DTYPES)}")
+        if kv_dtype == "uint8":
+            # The presses score K as floats; a 1-byte pool has no compiled press kernel,
+            # so it is refused here rather than on its first compress call.
+            raise NotImplementedError("device pools need a float KV dtype (float16, bfloat16, "
+                                      "float32); bytes_per_element=1 pools are ledger-only")
         self.kv_dtype = kv_dtype
         self.torch_dtype = getattr(torch, kv_dtype)
         self.config = config
@@ -199,7 +204,10 @@ class _NativePool:
         self.max_blocks = -(-max_tokens_per_handle // block_size)
         block_bytes = config.bytes_per_token * block_size
         if num_blocks is None:
-            num_blocks = capacity_bytes // block_bytes + max_handles
+            # One partial block per live handle (two in legacy mode: the retained raw row
+            # and the live row), so byte admission implies block availability.
+            partial = 2 if mode is PoolMode.LEGACY_ZOMBIE else 1
+            num_blocks = capacity_bytes // block_bytes + partial * max_handles
         self.num_blocks = int(num_blocks)
         self.arena = torch.empty(self.num_blocks * block_bytes, dtype=torch.uint8,
                                  device=self.device)
@@ -368,7 +376,8 @@ class KVCachePool:
     * ``max_handles`` -- live handles the device block tables hold.
     * ``max_tokens_per_handle`` -- longest cache a handle may reach.
     * ``num_blocks`` -- arena blocks (default ``capacity // block_bytes +
-      max_handles``, so byte admission implies block availability).
+      max_handles``, twice ``max_handles`` in legacy mode, so byte admission
+      implies block availability).
     * ``kv_dtype`` -- element type the presses interpret ("float16",
       "bfloat16", "float32"; default from ``bytes_per_element``).
     * ``compressor`` -- the ``CompressorSpec`` ``transition_compressed`` uses.
@@ -543,9 +552,19 @@ class KVCachePool:
             if h.handle_id in seen:
                 raise ValueError("handle repeated in batch")
             seen.add(h.handle_id)
+        expect = [compressed_spec(h.spec, comp) for h in handles]
         if new_specs is None:
-            new_specs = [compressed_spec(h.spec, comp) for h in handles]
+            new_specs = expect
         new_specs = list(new_specs)
+        if len(new_specs) != len(handles):
+            raise ValueError("new_specs needs one spec per handle")
+        if self._native is not None:
+            # The device keeps exactly compressed_spec(h.spec, comp) rows per segment;
+            # a different caller spec would desynchronise the ledger from the payload.
+            for h, want, got in zip(handles, expect, new_specs):
+                if [s.token_count for s in want.segments] != [s.token_count for s in got.segments]:
+                    raise ValueError(f"new_spec of handle {h.handle_id} does not match "
+                                     "compressed_spec(handle.spec, comp)")
         if self.mode is PoolMode.LEGACY_ZOMBIE:
             avail = self.available_bytes
             for spec in new_specs:
@@ -699,6 +718,10 @@ class KVCachePool:
             if tuple(t.shape) != want or t.dtype != nv.torch_dtype or t.device != nv.device \
                     or not t.is_contiguous():
                 raise ValueError(f"k and v must be contiguous {nv.kv_dtype} CUDA tensors {want}")
+        if tok_begin is not None:
+            tok_begin = [int(x) for x in tok_begin]
+            if len(tok_begin) != len(handles):
+                raise ValueError("tok_begin needs one entry per handle")
         cu = [0]
         for n in lens:
             cu.append(cu[-1] + n)
@@ -717,6 +740,10 @@ class KVCachePool:
             if tuple(t.shape) != want or t.dtype != nv.torch_dtype or t.device != nv.device \
                     or not t.is_contiguous():
                 raise ValueError(f"k and v must be contiguous {nv.kv_dtype} CUDA tensors {want}")
+        if positions is not None:
+            positions = [int(x) for x in positions]
+            if len(positions) != len(handles):
+                raise ValueError("positions needs one entry per handle")
         if handles:
             nv.write_kv(layer, [h.handle_id for h in handles], positions, k, v)
 
@@ -820,6 +847,14 @@ class KVCachePool:
         nv._check(nv.lib.fc_pool_last_profile(nv.ptr, ctypes.byref(prof)))
         return {"press_ms": prof.press_ms, "free_ms": prof.free_ms, "total_ms": prof.total_ms,
                 "press_launches": prof.press_launches, "total_launches": prof.total_launches}
+
+    def last_paths(self) -> dict:
+        """Press launches of the most recent compress call per implementation:
+        ``{"tc": tcgen05 kernels, "simt": SIMT press kernels, "chunk": chunk fold}``."""
+        nv = self._need_native()
+        out = (ctypes.c_int64 * 3)()
+        nv._check(nv.lib.fc_pool_last_paths(nv.ptr, out))
+        return {"tc": int(out[0]), "simt": int(out[1]), "chunk": int(out[2])}
 
     def synchronize(self) -> None:
         if self._native is not None:

@@ -142,6 +142,7 @@ def test_knorm_per_segment_and_repeat_errors(cuda):
     raws = [osynth.to_f32(_stored_np(pool.load_tokens(h), "float16"), "float16") for h in hs]
     comp = CompressorSpec(factor=4, press=PressKind.KNORM, per_segment=True)
     res = pool.compress_batch(hs, comp, 1.0, return_indices=True)
+    assert pool.last_paths() == {"tc": 0, "simt": 1, "chunk": 0}   # the fused Knorm kernel
     for i, segs in enumerate(([64, 40], [33])):
         want = opress.select(opress.knorm_scores(raws[i][1, 0, 1], 2), segs, 4, per_segment=True)
         assert res.kept_idx[i][1, 1].cpu().numpy().tolist() == want.tolist()
@@ -205,6 +206,15 @@ def test_append_and_churn_block_tables(cuda):
     assert 0.0 <= st.fragmentation < 1.0
 
 
+def _assert_path(pool, tc: bool):
+    """The press implementation the last compress call launched (fc_pool_last_paths)."""
+    paths = pool.last_paths()
+    if tc:
+        assert paths["tc"] >= 1 and paths["simt"] == 0, paths
+    else:
+        assert paths["tc"] == 0 and paths["simt"] >= 1, paths
+
+
 def _snap_inputs(n, L, hq, w, D, seed, device, dtype):
     g = torch.Generator().manual_seed(seed)
     q = torch.randn((n, L, hq, w, D), generator=g, dtype=torch.float32).to(getattr(torch, dtype))
@@ -231,6 +241,7 @@ def test_snapkv_parity(cuda, dtype, L, H, gq, D, specs, w, p):
     q = _snap_inputs(len(specs), L, H * gq, w, D, 5, cuda, dtype)
     comp = CompressorSpec(factor=4, press=PressKind.SNAPKV, window=w, pool_kernel=p)
     res = pool.compress_batch(hs, comp, 1.0, q_window=q, return_indices=True, return_scores=True)
+    _assert_path(pool, tc=dtype != "float32" and w == 32)
     qn = q.float().cpu().numpy()
     for i, s in enumerate(specs):
         kv32 = osynth.to_f32(raw[i], dtype)
@@ -275,6 +286,7 @@ def test_expected_attention_parity(cuda, dtype, L, H, gq, D, specs, ns):
     comp = CompressorSpec(factor=4, press=PressKind.EXPECTED_ATTENTION, n_sink=ns)
     res = pool.compress_batch(hs, comp, 1.0, mean_q=mu.to(cuda), cov_q=cov.contiguous().to(cuda),
                               return_indices=True, return_scores=True)
+    _assert_path(pool, tc=dtype != "float32" and D == 128)
     for i, s in enumerate(specs):
         kv32 = osynth.to_f32(raw[i], dtype)
         k_r = opress.kept_budget([x for x in s if x > 0], 4)
@@ -344,3 +356,64 @@ def test_churn_waves_conserve_and_free_everything(cuda):
     bs = pool.block_stats()
     assert pool.current_bytes == 0 and bs.used_blocks == 0 and bs.free_blocks == bs.num_blocks
     assert 0.0 <= st.max_fragmentation < 1.0
+
+
+@pytest.mark.parametrize("press", [PressKind.SNAPKV, PressKind.EXPECTED_ATTENTION])
+@pytest.mark.parametrize("gq", [1, 2])
+def test_tensor_core_presses_per_segment(cuda, press, gq):
+    """per_segment=True on the tcgen05 kernels: top-ceil(n_seg/f) per modality segment
+    (mirrors compressed_spec exactly, kv.py:173-194)."""
+    dtype, L, H, D = "float16", 2, 2, 128
+    cfg = _model(dtype, L, H, D)
+    pool = _make_pool(cuda, cfg, dtype, num_q_heads=H * gq)
+    specs = [(576, 300), (0, 700), (200, 0), (37, 1900)]
+    hs = pool.allocate_batch(list(range(len(specs))), [split_modalities(*s) for s in specs], 0.0)
+    pool.synth_fill(hs, seed=31)
+    raw = [_stored_np(pool.load_tokens(h), dtype) for h in hs]
+    n, hq = len(specs), H * gq
+    kw = {}
+    if press is PressKind.SNAPKV:
+        q = _snap_inputs(n, L, hq, 32, D, 6, cuda, dtype)
+        kw["q_window"] = q
+        comp = CompressorSpec(factor=4, press=press, window=32, pool_kernel=7, per_segment=True)
+    else:
+        gen = torch.Generator().manual_seed(10)
+        mu = (torch.randn((n, L, hq, D), generator=gen) / D ** 0.5).float()
+        a = torch.randn((n, L, hq, D, D), generator=gen)
+        cov = (a @ a.transpose(-1, -2) / D).float().contiguous()
+        kw.update(mean_q=mu.to(cuda), cov_q=cov.to(cuda))
+        comp = CompressorSpec(factor=4, press=press, n_sink=4, per_segment=True)
+    res = pool.compress_batch(hs, comp, 1.0, return_indices=True, return_scores=True, **kw)
+    _assert_path(pool, tc=True)
+    for i, s in enumerate(specs):
+        kv32 = osynth.to_f32(raw[i], dtype)
+        segs = [x for x in s if x > 0]
+        assert hs[i].spec.total_tokens == opress.kept_budget(segs, 4)
+        for layer in range(L):
+            for h in range(H):
+                sl = slice(h * gq, (h + 1) * gq)
+                if press is PressKind.SNAPKV:
+                    want = opress.snapkv_scores(kv32[layer, 0, h], q.float().cpu().numpy()[i, layer, sl], 32, 7)
+                else:
+                    want = opress.expected_attention_scores(kv32[layer, 0, h], kv32[layer, 1, h],
+                                                            mu[i, layer, sl].numpy(),
+                                                            cov[i, layer, sl].numpy(), 4)
+                got = res.scores[i][layer, h].cpu().numpy().astype(np.float64)
+                fin = np.isfinite(want)
+                assert np.array_equal(np.isfinite(got), fin)
+                rel = np.abs(got[fin] - want[fin]) / np.abs(want[fin])
+                assert rel.max() <= SCORE_RTOL, (i, layer, h, rel.max())
+                kept = res.kept_idx[i][layer, h].cpu().numpy()
+                # per segment: each segment's kept set is its own top-ceil(n/4)
+                start = 0
+                for n_seg in segs:
+                    part = kept[(kept >= start) & (kept < start + n_seg)] - start
+                    k_seg = opress.kept_budget([n_seg], 4)
+                    assert len(part) == k_seg, (i, layer, h, n_seg)
+                    assert opress.kept_set_mismatch(part, want[start:start + n_seg], k_seg,
+                                                    SCORE_RTOL) is None
+                    start += n_seg
+        got_c = _stored_np(pool.load_tokens(hs[i]), dtype)
+        want_c = opress.gather_kept(raw[i], res.kept_idx[i].cpu().numpy())
+        assert np.array_equal(got_c.view(np.uint8), want_c.view(np.uint8))
+    pool.verify_conservation()
