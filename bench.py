@@ -26,6 +26,7 @@ data path, NCCL only for the barrier / max-over-ranks timing.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -531,16 +532,38 @@ def run_prefill_bench(args, rank, world, local_rank):
 
 
 def run_ours(args, rank, world, local_rank):
+    """The headline press config, then (default c2 run) the c3 / c4w legs in the same
+    process, each with its own roofline, clocks and sampled parity."""
     import torch
 
-    from paper_2503_08461_b200 import KVCachePool, _native, compressed_spec, kv_bytes
+    result = press_leg(args, args.config, rank, world, local_rank, with_e2e=args.e2e_steps > 0)
+    legs = [x for x in args.legs.split(",") if x and x != args.config] if args.legs else []
+    if legs:
+        result["legs"] = {}
+        for name in legs:
+            gc.collect()                # pools and their handles reference each other
+            torch.cuda.empty_cache()
+            leg = press_leg(args, name, rank, world, local_rank, with_e2e=False)
+            result["legs"][name] = {k: leg[k] for k in (
+                "value", "unit", "ms_per_step", "scaling", "dtype", "config", "hbm_gbs_per_gpu",
+                "kept_tokens_per_s", "roofline", "gpu_launches", "clocks", "parity", "paths")}
+    return result
+
+
+def press_leg(args, name, rank, world, local_rank, with_e2e):
+    """One press config: W warm-up + K timed compress_batch steps over a batch resident in the
+    pool (CUDA events on the launch stream, max over ranks), then one untimed extra batch
+    checked against the oracle on a sample of segments (``parity``)."""
+    import torch
+
+    from paper_2503_08461_b200 import KVCachePool, compressed_spec, kv_bytes
 
     from paper_2503_08461_b200 import shard
 
     device = torch.device("cuda", local_rank)
     torch.cuda.set_device(device)
-    cfg, dtype, specs, comp = workload(args.config)
-    strong = args.config in STRONG
+    cfg, dtype, specs, comp = workload(name)
+    strong = name in STRONG
     job_kept = sum(compressed_spec(s, comp).total_tokens for s in specs) * (1 if strong else world)
     if strong:  # fixed total work, LPT-balanced request shards
         total_tokens = sum(s.total_tokens for s in specs)
@@ -549,18 +572,18 @@ def run_ours(args, rank, world, local_rank):
     raw_tokens = sum(s.total_tokens for s in specs)
     job_tokens = total_tokens if strong else raw_tokens * world
     cap = sum(kv_bytes(cfg, s.total_tokens) for s in specs)
+    hq = Q_HEADS.get(name, cfg.num_kv_heads)
     pool = KVCachePool(cfg, cap, device=device, kv_dtype=dtype, max_handles=max(64, 2 * n),
                        max_tokens_per_handle=max(s.total_tokens for s in specs) + 64,
-                       num_q_heads=Q_HEADS.get(args.config, cfg.num_kv_heads))
+                       num_q_heads=hq)
     pool.set_profiling(True)
-    ins = press_inputs(comp, cfg, n, device, torch, seed=1234 + rank,
-                       hq=Q_HEADS.get(args.config, cfg.num_kv_heads))
+    ins = press_inputs(comp, cfg, n, device, torch, seed=1234 + rank, hq=hq)
     rids = [rank * 1_000_000 + i for i in range(n)]
     stream = torch.cuda.current_stream(device)
 
     def fill():
         hs = pool.allocate_batch(rids, specs, 0.0)
-        pool.synth_fill(hs, seed=17)
+        pool.synth_fill(hs, seed=SYNTH_SEED)
         return hs
 
     press_ms, step_ms, launches, press_launches = [], [], 0, 0
@@ -586,15 +609,20 @@ def run_ours(args, rank, world, local_rank):
             press_launches += prof["press_launches"]
             pool.release_batch(hs, 2.0)
         torch.cuda.synchronize(device)
+    paths = pool.last_paths()
     if world > 1:
         torch.distributed.barrier()
     total_ms = sum(step_ms)
     max_ms = _allreduce(total_ms, "max", device)
     value = job_tokens * args.steps / (max_ms / 1e3)
-    abytes = alg_bytes(cfg, specs, comp, Q_HEADS.get(args.config))
+    abytes = alg_bytes(cfg, specs, comp, Q_HEADS.get(name))
     peak, peak_kind = measured_peak()
     press_avg = statistics.mean(press_ms)
     achieved = abytes / (press_avg / 1e3) / 1e9
+    kernel = {"knorm": "press_kernel<KNORM> (score + top-k + in-place compaction)",
+              "snapkv": "snapkv_tc_kernel (tcgen05 window QK^T + softmax/pool + top-k + compaction)",
+              "expected_attention": "ea_tc_kernel (tcgen05 K.[Sigma;mu] + softmax*|V| + top-k + "
+                                    "compaction)"}.get(comp.press.value, "press kernel")
     result = {
         "metric": "compressed KV tokens/s",
         "value": value,
@@ -609,7 +637,7 @@ def run_ours(args, rank, world, local_rank):
         "dtype": {"float16": "f16", "bfloat16": "bf16", "float32": "f32"}[dtype],
         "data": "synthetic (deterministic counter-based KV generator, oracle/synth.py)",
         "config": {
-            "workload": f"{args.config}: {CONFIGS[args.config]}",
+            "workload": f"{name}: {CONFIGS[name]}",
             "press": comp.press.value, "factor": comp.factor, "requests_per_gpu": n,
             "raw_tokens_per_gpu": raw_tokens,
             "parallelism": f"request-sharded x{world} ({'LPT shards of one batch' if strong else 'one batch per GPU'}; no data-path collective)",
@@ -620,9 +648,9 @@ def run_ours(args, rank, world, local_rank):
         "hbm_gbs_per_gpu": abytes * args.steps / (max_ms / 1e3) / 1e9,
         "kept_tokens_per_s": job_kept * args.steps / (max_ms / 1e3),
         "roofline": {
-            "bound": "hbm", "kernel": "press_kernel (score + top-k + in-place compaction)",
+            "bound": "hbm", "kernel": kernel,
             "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": traffic_from_profile(args.config),
+            "frac": achieved / peak, "traffic": traffic_from_profile(name),
             "frac_of_nominal_8tbs": achieved / 8000.0,
             "peak_note": "peak = MEASURED_PEAKS.json hbm_gbs, a 1:1 read/write copy; the press "
                          "mix is read-heavy (Knorm 2:1), which HBM serves faster than a copy, so "
@@ -632,12 +660,45 @@ def run_ours(args, rank, world, local_rank):
             "press_ms": press_avg,
         },
         "gpu_launches": launches,
+        "paths": paths,
         "clocks": clocks.summary(),
     }
-    if args.e2e_steps > 0:
+    if args.parity_segments > 0:
+        result["parity"] = sampled_parity(pool, fill, specs, comp, ins, dtype, rids,
+                                          args.parity_segments, device, world)
+    if with_e2e:
         result["e2e"] = run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world,
                                 job_tokens)
+    del pool
     return result
+
+
+SYNTH_SEED = 17
+
+
+def sampled_parity(pool, fill, specs, comp, ins, dtype, rids, n_segments, device, world):
+    """Untimed: one more batch, compressed with indices + scores, checked on ``n_segments``
+    sampled (request, layer, head) segments against the CPU oracle (oracle/parity.py, the
+    checker only), summed over ranks."""
+    import torch
+
+    from oracle import parity
+
+    hs = fill()
+    res = pool.compress_batch(hs, comp, 1.0, return_indices=True, return_scores=True, **ins)
+    t0 = time.perf_counter()
+    rep = parity.check_batch(pool, hs, specs, comp, res, dtype=dtype, seed=SYNTH_SEED, keys=rids,
+                             inputs=ins, n_segments=n_segments)
+    rep["check_s"] = time.perf_counter() - t0
+    pool.verify_conservation()
+    pool.release_batch(hs, 2.0)
+    del res
+    torch.cuda.synchronize(device)
+    if world > 1:
+        rep["segments"] = int(_allreduce(float(rep["segments"]), "sum", device))
+        rep["mismatches"] = int(_allreduce(float(rep["mismatches"]), "sum", device))
+        rep["max_score_rel_err"] = _allreduce(rep["max_score_rel_err"], "max", device)
+    return rep
 
 
 E2E_MAX_PINNED_BYTES = 64 * 10 ** 9
@@ -679,7 +740,7 @@ def run_e2e(args, pool, cfg, dtype, specs, comp, ins, rids, device, world, job_t
     shapes = [(cfg.num_layers, 2, cfg.num_kv_heads, s.total_tokens, cfg.head_dim) for s in specs]
     tdt = getattr(torch, dtype)
     hs = pool.allocate_batch(rids, specs, 0.0)
-    pool.synth_fill(hs, seed=17)
+    pool.synth_fill(hs, seed=SYNTH_SEED)
     host = []
     for h, shp in zip(hs, shapes):
         buf = torch.empty(shp, dtype=tdt, pin_memory=True)
@@ -846,7 +907,7 @@ def run_reference(args):
     cb["value"] = value
     return {
         "metric": "compressed KV tokens/s", "value": value, "unit": "tokens/s", "n_gpus": 0,
-        "steps": args.steps, "warmup": args.warmup,
+        "ranks": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f16" if dtype == "float16" else dtype,
         "data": "synthetic", "impl": "reference",
@@ -858,6 +919,35 @@ def run_reference(args):
     }
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """``--gpus N`` without a torchrun environment: re-exec this script as N ranks under
+    ``torch.distributed.run`` (one process per GPU, NCCL). On a box with fewer GPUs than N
+    the ranks share the visible GPUs over gloo (a multi-rank path check, flagged in the
+    output). NCCL's INIT log (communicator size per rank) goes to stderr."""
+    import subprocess
+
+    import torch
+
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    if torch.cuda.device_count() < args.gpus:
+        env["FASTCACHE_DIST_BACKEND"] = "gloo"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -867,21 +957,36 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--legs", default=None,
+                    help="extra press configs measured in the same run (default for c2: c3,c4w)")
+    ap.add_argument("--parity-segments", type=int, default=64,
+                    help="sampled (request, layer, head) segments checked against the oracle "
+                         "after the timed region (0 = off)")
     args = ap.parse_args()
+    if args.legs is None:
+        args.legs = "c3,c4w" if args.config == "c2" else ""
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        raise SystemExit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+                         f"(torchrun --nproc-per-node {args.gpus}) or drop WORLD_SIZE")
     if args.impl == "reference":
         if rank == 0:
             print(json.dumps(run_reference(args)), flush=True)
         return
     import torch
 
-    # FASTCACHE_DIST_BACKEND=gloo lets several ranks share one GPU (multi-rank path tests on
-    # a single-GPU box); the default is one rank per GPU over NCCL.
+    # FASTCACHE_DIST_BACKEND=gloo lets several ranks share one GPU (multi-rank path checks on
+    # a box with fewer GPUs than ranks); the default is one rank per GPU over NCCL.
     backend = os.environ.get("FASTCACHE_DIST_BACKEND", "nccl")
+    shared = torch.cuda.device_count() < world
     local_rank = local_rank % max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local_rank)
@@ -899,6 +1004,12 @@ def main():
         result = run_prefill_bench(args, rank, world, local_rank)
     else:
         result = run_ours(args, rank, world, local_rank)
+    if world > 1:
+        result.setdefault("config", {})["backend"] = backend
+        if shared:
+            result["config"]["shared_device"] = (
+                f"{world} ranks on {torch.cuda.device_count()} visible GPU(s) over {backend}: a "
+                "multi-rank path check, not a scaling number")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cfg, dtype, specs, comp = workload(args.config if args.config not in ("c5", "c2d", "c2p") else "c2")
         result["cpu_baseline"] = cpu_reference(args, cfg, dtype, specs, comp)
