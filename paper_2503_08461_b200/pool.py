@@ -415,6 +415,7 @@ class KVCachePool:
         self._retained_handles = 0
         self._next_id = 0
         self.zombie_coexistence_observed = False
+        self._deferred: set[int] = set()     # device-compressed, ledger transition pending
         self.compressor = compressor or CompressorSpec()
         self.num_q_heads = num_q_heads or config.num_kv_heads
         self._native: _NativePool | None = None
@@ -504,6 +505,18 @@ class KVCachePool:
         self._transition_ledger(handle, new_spec, now)
         return handle
 
+    def commit_compressed(self, handles: Sequence[CacheHandle], new_specs: Sequence[KVCacheSpec],
+                          now: float) -> None:
+        """Ledger half of a ``compress_batch(..., defer_ledger=True)``: the reference
+        per-member transitions (pool.py:167-192), in the given order, at ``now``."""
+        handles, new_specs = list(handles), list(new_specs)
+        for h in handles:
+            if h.handle_id not in self._deferred:
+                raise InvalidState(f"handle {h.handle_id} has no deferred compression")
+        for h, spec in zip(handles, new_specs):
+            self._transition_ledger(h, spec, now)
+            self._deferred.discard(h.handle_id)
+
     def _transition_ledger(self, handle: CacheHandle, new_spec: KVCacheSpec, now: float) -> None:
         compressed = kv_bytes(self.config, new_spec.total_tokens)
         if self.mode is PoolMode.POOLED:
@@ -523,7 +536,8 @@ class KVCachePool:
     def compress_batch(self, handles: Sequence[CacheHandle], comp: CompressorSpec | None = None,
                        now: float = 0.0, *, q_window=None, mean_q=None, cov_q=None,
                        return_indices: bool = False, return_scores: bool = False,
-                       new_specs: Sequence[KVCacheSpec] | None = None, host_kv=None):
+                       new_specs: Sequence[KVCacheSpec] | None = None, host_kv=None,
+                       defer_ledger: bool = False):
         """Compress many RAW handles in one batched device pass, then transition them.
 
         ``comp.press`` picks the scorer; every member keeps exactly
@@ -542,12 +556,19 @@ class KVCachePool:
         for pooled Knorm / SnapKV only the K planes and the kept V rows cross
         PCIe (``fc_pool_compress_host_batch``). The tensors must stay alive
         until the pool's stream has run this call.
+
+        ``defer_ledger=True`` (device pools): run the device pass now but leave the
+        host ledger transitions to a later ``commit_compressed(handles, specs, now)``
+        -- a serving engine charges the measured press time and transitions at the
+        stage's completion time, as the reference does (engine.py:501-510). Returns
+        the new specs (and the ``CompressResult`` as ``(specs, result)`` when
+        indices/scores are requested).
         """
         comp = comp or self.compressor
         handles = list(handles)
         seen = set()
         for h in handles:
-            if h.state is not HandleState.RAW:
+            if h.state is not HandleState.RAW or h.handle_id in self._deferred:
                 raise InvalidState(f"transition requires a raw handle, got {h.state}")
             if h.handle_id in seen:
                 raise ValueError("handle repeated in batch")
@@ -578,6 +599,11 @@ class KVCachePool:
                                            return_indices, return_scores, host_kv)
         elif host_kv is not None:
             raise nat.NativeUnavailable("host_kv needs a device pool (pass device=...)")
+        if defer_ledger:
+            if self._native is None:
+                raise ValueError("defer_ledger needs a device pool")
+            self._deferred.update(h.handle_id for h in handles)
+            return (new_specs, result) if (return_indices or return_scores) else new_specs
         for h, spec in zip(handles, new_specs):
             self._transition_ledger(h, spec, now)
         if return_indices or return_scores:
