@@ -177,15 +177,16 @@ __device__ __forceinline__ float block_reduce(float v, bool is_max, SelectScratc
 template <typename T, int D>
 __device__ void score_snapkv(const char* __restrict__ seg, const Geom& g, const int32_t* s_tab,
                              int T_len, const PressParams& pp, const T* __restrict__ qwin,
-                             float* sc, float* scratch, float* __restrict__ ws, SelectScratch& ss) {
+                             float* sc, float* scratch, float* s1, float* __restrict__ ws,
+                             SelectScratch& ss) {
   constexpr int kTile = 32;
   const int w = pp.window;
   const int gq = pp.num_q_heads / g.H;
   const int n_keep = T_len - w;  // scored positions
   float* qs = scratch;                         // [w][D+1]
   float* ks = qs + w * (D + 1);                // [kTile][D+1]
-  float* s1 = ks + kTile * (D + 1);            // [T]
-  float* mz = s1 + ((T_len + 3) & ~3);         // [2][w]
+  float* mz = ks + kTile * (D + 1);            // [2][w]
+  // s1 [T]: SMEM after mz, or a global spill row for segments beyond the SMEM plan
   const float inv_sqrt_d = 1.0f / sqrtf((float)D);
   for (int t = threadIdx.x; t < T_len; t += kThreads) sc[t] = 0.f;
   for (int qh = 0; qh < gq; ++qh) {
@@ -269,7 +270,7 @@ template <typename T, int D>
 __device__ void score_ea(const char* __restrict__ seg, const Geom& g, const int32_t* s_tab,
                          int T_len, const PressParams& pp, const float* __restrict__ mu_g,
                          const float* __restrict__ cov_g, float* sc, float* scratch,
-                         SelectScratch& ss) {
+                         float* zt, SelectScratch& ss) {
   constexpr int kTokW = 4;                       // tokens per warp per sweep
   constexpr int kTile = kWarps * kTokW;          // 32 tokens per CTA sweep
   constexpr int kC = D / 32;                     // columns per lane
@@ -278,7 +279,7 @@ __device__ void score_ea(const char* __restrict__ seg, const Geom& g, const int3
   float* sig = scratch;                          // [D][D]
   float* mu = sig + D * D;                       // [D]
   float* kt = mu + D;                            // [kTile][D]
-  float* zt = kt + kTile * D;                    // [T]
+  // zt [T]: SMEM after kt, or a global spill row for segments beyond the SMEM plan
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float inv_sqrt_d = 1.0f / sqrtf((float)D);
   const float inv_2d = 1.0f / (2.0f * (float)D);
@@ -375,35 +376,57 @@ struct SmemPlan {
 
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
+// spill: the segment is longer than the SMEM plan allows. Block tables are then read
+// straight from global memory, and the T-sized arrays (scores -> keys -> kept indices,
+// SnapKV's window mean, EA's logits) live in a per-CTA global row (L2-resident) instead
+// of SMEM; nothing else changes. spill_floats() is that row's length.
 __host__ __device__ inline SmemPlan smem_plan(int kind, int max_T, int bs, int D, int window,
-                                              bool in_place, int row_bytes = 256) {
+                                              bool in_place, int row_bytes = 256,
+                                              bool spill = false) {
   SmemPlan p;
   p.nb = (max_T + bs - 1) / bs;
-  p.tab_bytes = align16(p.nb * 4) * (in_place ? 1 : 2);
-  p.sc_bytes = align16(max_T * 4);
+  p.tab_bytes = spill ? 0 : align16(p.nb * 4) * (in_place ? 1 : 2);
+  p.sc_bytes = spill ? 0 : align16(max_T * 4);
   p.scratch_bytes = 0;
   p.cbuf_bytes = (FC_KNORM_ASYNC && kind == FC_PRESS_KNORM) ? kKnBufs * kKnRanks * 2 * row_bytes : 0;
+  const int t_arr = spill ? 0 : ((max_T + 3) & ~3);
   if (kind == FC_PRESS_SNAPKV)
-    p.scratch_bytes = align16((window * (D + 1) + 32 * (D + 1) + ((max_T + 3) & ~3) + 2 * window) * 4);
+    p.scratch_bytes = align16((window * (D + 1) + 32 * (D + 1) + 2 * window + t_arr) * 4);
   else if (kind == FC_PRESS_EXPECTED_ATTENTION)
-    p.scratch_bytes = align16((D * D + D + kWarps * 4 * D + max_T) * 4);
+    p.scratch_bytes = align16((D * D + D + kWarps * 4 * D + t_arr) * 4);
   return p;
 }
 
-template <typename T, int D, int KIND>
+__host__ __device__ inline int64_t spill_floats(int kind, int max_T) {
+  const int64_t t = (max_T + 3) & ~3;
+  return kind == FC_PRESS_KNORM ? t : 2 * t;
+}
+
+constexpr int kSmemLimit = 220 * 1024;   // SIMT press plans above this take the spill variant
+constexpr int kSpillCtasPerSm = 2;
+
+template <typename T, int D, int KIND, bool kSpill>
 __global__ void __launch_bounds__(kThreads, KIND == FC_PRESS_KNORM ? FC_KN_MINB : 2)
     press_kernel(char* __restrict__ arena, const int32_t* __restrict__ src_table,
                  const int32_t* __restrict__ dst_table, const Geom g,
                  const __grid_constant__ PressBatch b, const PressParams pp,
                  const fc_press_inputs in, const fc_press_outputs out, float* __restrict__ ws,
-                 int64_t ws_per_cta, int n_items) {
+                 int64_t ws_per_cta, int n_items, float* __restrict__ spill) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SelectScratch ss;
-  const SmemPlan plan = smem_plan(KIND, b.max_T, g.bs, D, pp.window, b.in_place != 0, D * (int)sizeof(T));
+  const SmemPlan plan = smem_plan(KIND, b.max_T, g.bs, D, pp.window, b.in_place != 0,
+                                  D * (int)sizeof(T), kSpill);
   int32_t* s_src = reinterpret_cast<int32_t*>(smem);
   int32_t* s_dst = b.in_place ? s_src : s_src + plan.tab_bytes / 8;
-  float* sc = reinterpret_cast<float*>(smem + plan.tab_bytes);
+  const int64_t t_pad = (b.max_T + 3) & ~3;
+  float* sc = kSpill ? spill + (int64_t)blockIdx.x * spill_floats(KIND, b.max_T)
+                     : reinterpret_cast<float*>(smem + plan.tab_bytes);
   float* scratch = reinterpret_cast<float*>(smem + plan.tab_bytes + plan.sc_bytes);
+  // SnapKV's window mean / EA's logits: after the fixed scratch in SMEM, or spilled
+  float* tarr = kSpill ? sc + t_pad
+                       : scratch + (KIND == FC_PRESS_SNAPKV
+                                        ? pp.window * (D + 1) + 32 * (D + 1) + 2 * pp.window
+                                        : D * D + D + kWarps * 4 * D);
   const int LH = g.L * g.H;
 
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -413,9 +436,14 @@ __global__ void __launch_bounds__(kThreads, KIND == FC_PRESS_KNORM ? FC_KN_MINB 
     const int T_len = q.T, K = q.K;
     const int nb = (T_len + g.bs - 1) / g.bs;
     __syncthreads();  // previous item's SMEM fully consumed
-    for (int i = threadIdx.x; i < nb; i += kThreads) {
-      s_src[i] = src_table[(int64_t)q.slot * g.max_bpr + i];
-      if (!b.in_place) s_dst[i] = dst_table[(int64_t)q.slot * g.max_bpr + i];
+    if (kSpill) {     // tables read in place (the kernel never writes them)
+      s_src = const_cast<int32_t*>(src_table) + (int64_t)q.slot * g.max_bpr;
+      s_dst = b.in_place ? s_src : const_cast<int32_t*>(dst_table) + (int64_t)q.slot * g.max_bpr;
+    } else {
+      for (int i = threadIdx.x; i < nb; i += kThreads) {
+        s_src[i] = src_table[(int64_t)q.slot * g.max_bpr + i];
+        if (!b.in_place) s_dst[i] = dst_table[(int64_t)q.slot * g.max_bpr + i];
+      }
     }
     if (threadIdx.x == 0) ss.first_drop = INT_MAX;
     __syncthreads();
@@ -428,13 +456,13 @@ __global__ void __launch_bounds__(kThreads, KIND == FC_PRESS_KNORM ? FC_KN_MINB 
       const int gq = pp.num_q_heads / g.H;
       const T* qwin = reinterpret_cast<const T*>(in.q_window) +
                       (((int64_t)q.q_idx * g.L + l) * pp.num_q_heads + (int64_t)h * gq) * pp.window * D;
-      score_snapkv<T, D>(seg, g, s_src, T_len, pp, qwin, sc, scratch,
+      score_snapkv<T, D>(seg, g, s_src, T_len, pp, qwin, sc, scratch, tarr,
                          ws + (int64_t)blockIdx.x * ws_per_cta, ss);
     } else {
       const int gq = pp.num_q_heads / g.H;
       const int64_t qoff = ((int64_t)q.q_idx * g.L + l) * pp.num_q_heads + (int64_t)h * gq;
       score_ea<T, D>(seg, g, s_src, T_len, pp, in.mean_q + qoff * D, in.cov_q + qoff * D * D, sc,
-                     scratch, ss);
+                     scratch, tarr, ss);
     }
     __syncthreads();
     if (out.scores) {
@@ -569,12 +597,23 @@ __global__ void __launch_bounds__(kThreads)
 // ---------------------------------------------------------------------------
 // host dispatch
 // ---------------------------------------------------------------------------
+// SnapKV SIMT window logits (ws[w][T] per CTA, up to 4 CTAs per SM) + the spill rows of
+// segments beyond the SMEM plan (kSpillCtasPerSm per SM).
+static int64_t snap_ws_floats(int kind, int window, int max_T) {
+  return kind == FC_PRESS_SNAPKV ? (int64_t)sm_count() * 4 * window * max_T : 0;
+}
+
+static bool needs_spill(const Geom& g, int kind, int window, int max_T, bool in_place) {
+  if (kind > FC_PRESS_EXPECTED_ATTENTION) return false;
+  return smem_plan(kind, max_T, g.bs, g.D, window, in_place, g.D * g.bpe).total() > kSmemLimit;
+}
+
 int64_t press_workspace_floats(const Geom& g, int kind, int window, int num_q_heads, int max_T) {
-  (void)g;
   (void)num_q_heads;
-  if (kind != FC_PRESS_SNAPKV) return 0;
-  const int sms = sm_count();
-  return (int64_t)sms * 4 * window * max_T;
+  int64_t n = snap_ws_floats(kind, window, max_T);
+  if (needs_spill(g, kind, window, max_T, /*in_place=*/false))
+    n += (int64_t)sm_count() * kSpillCtasPerSm * spill_floats(kind, max_T);
+  return n;
 }
 
 template <typename T, int D, int KIND>
@@ -630,24 +669,39 @@ static fc_status launch_one(const Geom& g, char* arena, const int32_t* src, int3
       return launch_one<T, D, KIND>(g, arena, src, dst, rest, pp, in, out, ws, ws_floats, stream, dry);
     }
   }
-  const SmemPlan plan = smem_plan(KIND, b.max_T, g.bs, D, pp.window, b.in_place != 0, D * (int)sizeof(T));
+  constexpr int kKind = KIND == FC_PRESS_KNORM ? FC_PRESS_KNORM
+                       : KIND == FC_PRESS_SNAPKV ? FC_PRESS_SNAPKV
+                                                 : FC_PRESS_EXPECTED_ATTENTION;
+  const bool spill = smem_plan(KIND, b.max_T, g.bs, D, pp.window, b.in_place != 0,
+                               D * (int)sizeof(T)).total() > kSmemLimit;
+  const SmemPlan plan = smem_plan(KIND, b.max_T, g.bs, D, pp.window, b.in_place != 0,
+                                  D * (int)sizeof(T), spill);
   const int smem = plan.total();
-  if (smem > 220 * 1024)
+  if (smem > kSmemLimit)
     return set_error(FC_ERR_UNSUPPORTED, "request of %d tokens exceeds the SMEM budget", b.max_T);
-  if (dry) return FC_OK;
-  auto kern = press_kernel<T, D, KIND == FC_PRESS_KNORM ? FC_PRESS_KNORM
-                                   : KIND == FC_PRESS_SNAPKV ? FC_PRESS_SNAPKV
-                                                             : FC_PRESS_EXPECTED_ATTENTION>;
+  const int sms = sm_count();
+  const int64_t snap_ws = snap_ws_floats(KIND, pp.window, b.max_T);
+  const int64_t spill_row = spill_floats(KIND, b.max_T);
+  if (dry) return FC_OK;   // the pool sizes the workspace (press_workspace_floats) next
+  if (spill && ws_floats - snap_ws < spill_row)
+    return set_error(FC_ERR_INVALID_STATE, "press workspace too small for the spill rows");
+  auto kern = spill ? press_kernel<T, D, kKind, true> : press_kernel<T, D, kKind, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute");
   int grid = n_items;
   int64_t ws_per_cta = 0;
   if (KIND == FC_PRESS_SNAPKV) {
     ws_per_cta = (int64_t)pp.window * b.max_T;
-    const int sms = sm_count();
-    grid = (int)std::min<int64_t>(n_items, std::min<int64_t>((int64_t)sms * 4, ws_floats / ws_per_cta));
+    grid = (int)std::min<int64_t>(n_items, std::min<int64_t>((int64_t)sms * 4, snap_ws / ws_per_cta));
   }
-  kern<<<grid, kThreads, smem, stream>>>(arena, src, dst, g, b, pp, in, out, ws, ws_per_cta, n_items);
+  float* spill_base = nullptr;
+  if (spill) {
+    spill_base = ws + snap_ws;
+    grid = (int)std::min<int64_t>(grid, std::min<int64_t>((int64_t)sms * kSpillCtasPerSm,
+                                                          (ws_floats - snap_ws) / spill_row));
+  }
+  kern<<<grid, kThreads, smem, stream>>>(arena, src, dst, g, b, pp, in, out, ws, ws_per_cta,
+                                         n_items, spill_base);
   note_launch();
   note_path(kPathSimt);
   return cuda_check(cudaGetLastError(), "press_kernel");

@@ -15,11 +15,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2503_08461_b200 import KVCachePool, _native, kv_bytes  # noqa: E402
 
-cfg, dtype, specs, comp = bench.workload(sys.argv[1] if len(sys.argv) > 1 else "c3")
+name = sys.argv[1] if len(sys.argv) > 1 else "c3"
+cfg, dtype, specs, comp = bench.workload(name)
+hq = bench.Q_HEADS.get(name, cfg.num_kv_heads)
 dev = torch.device("cuda", 0)
 pool = KVCachePool(cfg, sum(kv_bytes(cfg, s.total_tokens) for s in specs), device=dev,
-                   kv_dtype=dtype, max_handles=256, max_tokens_per_handle=4096)
-ins = bench.press_inputs(comp, cfg, len(specs), dev, torch, seed=1)
+                   kv_dtype=dtype, max_handles=256, max_tokens_per_handle=9000, num_q_heads=hq)
+ins = bench.press_inputs(comp, cfg, len(specs), dev, torch, seed=1, hq=hq)
 for rep in range(3):
     hs = pool.allocate_batch(list(range(len(specs))), specs, 0.0)
     pool.synth_fill(hs, seed=1)

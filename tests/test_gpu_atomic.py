@@ -4,8 +4,8 @@ The reference pool is strict: every check runs before any mutation
 (reference pkg/src/kvservesim/pool.py:147-165 allocate, :167-192 transition,
 :194-211 append). These tests force each refusal the device path can hit
 *after* the Python-level checks -- block-pool exhaustion on append, a press
-launch plan the SMEM budget refuses (pooled split batches and legacy
-out-of-place compress) -- and check that block tables, free-block count,
+without a launch plan (pooled, and legacy out-of-place compress whose pops
+precede the press) -- and check that block tables, free-block count,
 payload and both ledgers are exactly as before. They also cover the serving
 pattern decode -> host-resident compress that regrows the kept-index scratch
 -> decode on one pool (a stale-pointer regression).
@@ -76,43 +76,42 @@ def test_append_block_exhaustion_mutates_nothing(cuda):
     pool.verify_conservation()
 
 
-def test_pooled_split_batch_refused_before_any_compaction(cuda):
-    """One request fits the ExpectedAttention tensor-core plan, the other exceeds every
-    SMEM plan: the whole batch is refused and the fitting request stays raw and intact."""
-    cfg = ModelConfig("m", 1, 2, 128, 2)
-    pool = KVCachePool(cfg, (1 << 17) * cfg.bytes_per_token, device=cuda, kv_dtype="float16",
-                       max_handles=8, max_tokens_per_handle=65536)
-    specs = [split_modalities(0, 300), split_modalities(0, 60000)]
-    hs = pool.allocate_batch([0, 1], specs, 0.0)
+def test_pooled_refused_batch_mutates_nothing(cuda):
+    """ExpectedAttention at head_dim 256 has no launch plan (the SIMT kernel's Sigma alone
+    exceeds the SMEM budget): the batch is refused by the dry run before anything moves."""
+    cfg = ModelConfig("m", 1, 2, 256, 2)
+    pool = KVCachePool(cfg, (1 << 14) * cfg.bytes_per_token, device=cuda, kv_dtype="float16",
+                       max_handles=8, max_tokens_per_handle=4096)
+    hs = pool.allocate_batch([0, 1], [split_modalities(0, 300), split_modalities(5, 900)], 0.0)
     pool.synth_fill(hs, seed=2)
     gen = torch.Generator().manual_seed(0)
-    mu = (torch.randn((2, 1, 2, 128), generator=gen) / 128 ** 0.5).float().to(cuda)
-    a = torch.randn((2, 1, 2, 128, 128), generator=gen)
-    cov = (a @ a.transpose(-1, -2) / 128).float().contiguous().to(cuda)
+    mu = (torch.randn((2, 1, 2, 256), generator=gen) / 16).float().to(cuda)
+    a = torch.randn((2, 1, 2, 256, 256), generator=gen)
+    cov = (a @ a.transpose(-1, -2) / 256).float().contiguous().to(cuda)
     comp = CompressorSpec(factor=4, press=PressKind.EXPECTED_ATTENTION, n_sink=4)
     before = _state(pool, hs)
     with pytest.raises(NotImplementedError):
         pool.compress_batch(hs, comp, 1.0, mean_q=mu, cov_q=cov)
     _same(before, _state(pool, hs))
     pool.verify_conservation()
-    # the fitting request alone compresses on the tensor-core kernel
-    pool.compress_batch(hs[:1], comp, 1.0, mean_q=mu[:1].contiguous(), cov_q=cov[:1].contiguous())
-    assert pool.last_paths()["tc"] == 1 and hs[0].spec.total_tokens == 75
+    # Knorm has a plan at head_dim 256: the same handles still compress afterwards
+    pool.compress_batch(hs, CompressorSpec(factor=4, press=PressKind.KNORM), 2.0)
+    assert [h.spec.total_tokens for h in hs] == [75, 227]
     pool.verify_conservation()
 
 
 def test_legacy_refusal_pops_nothing(cuda):
     """Legacy compress pops destination blocks before the press: a refused launch plan must
     be caught first (no leaked blocks, raw rows still mapped)."""
-    cfg = ModelConfig("m", 1, 1, 64, 4)
-    pool = KVCachePool(cfg, (1 << 17) * cfg.bytes_per_token, PoolMode.LEGACY_ZOMBIE, device=cuda,
-                       kv_dtype="float32", max_handles=8, max_tokens_per_handle=65536)
-    hs = pool.allocate_batch([0, 1], [split_modalities(0, 100), split_modalities(0, 60000)], 0.0)
+    cfg = ModelConfig("m", 1, 1, 256, 4)
+    pool = KVCachePool(cfg, (1 << 14) * cfg.bytes_per_token, PoolMode.LEGACY_ZOMBIE, device=cuda,
+                       kv_dtype="float32", max_handles=8, max_tokens_per_handle=4096)
+    hs = pool.allocate_batch([0, 1], [split_modalities(0, 100), split_modalities(0, 600)], 0.0)
     pool.synth_fill(hs, seed=3)
     gen = torch.Generator().manual_seed(1)
-    mu = (torch.randn((2, 1, 1, 64), generator=gen) / 8).float().to(cuda)
-    a = torch.randn((2, 1, 1, 64, 64), generator=gen)
-    cov = (a @ a.transpose(-1, -2) / 64).float().contiguous().to(cuda)
+    mu = (torch.randn((2, 1, 1, 256), generator=gen) / 16).float().to(cuda)
+    a = torch.randn((2, 1, 1, 256, 256), generator=gen)
+    cov = (a @ a.transpose(-1, -2) / 256).float().contiguous().to(cuda)
     comp = CompressorSpec(factor=4, press=PressKind.EXPECTED_ATTENTION, n_sink=4)
     before = _state(pool, hs)
     with pytest.raises(NotImplementedError):
