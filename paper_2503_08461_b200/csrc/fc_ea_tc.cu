@@ -25,6 +25,7 @@
 // Algorithmic bytes per segment: R + 2C + (D + D^2) * 4.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include <cstring>
@@ -54,7 +55,9 @@ namespace ea {
 
 constexpr int kD = 128;
 constexpr int kStages = 3;                      // TMA ring depth (GQA: 2, see ea_stages)
-__host__ __device__ constexpr int ea_stages(bool gqa) { return gqa ? 2 : kStages; }
+__host__ __device__ constexpr int ea_stages(bool gqa, bool spill = false) {
+  return gqa && !spill ? 2 : kStages;
+}
 constexpr int kTileM = 128;
 constexpr int kBRows = 144;                     // 128 Sigma^T rows + mu + 15 zero rows
 #ifndef FC_EA_CITEMS  // compactor 16-B loads in flight per thread per chunk
@@ -80,7 +83,7 @@ using Consumers = NamedGroup<kConsumerFirst, 1>;
 using Compactors = NamedGroup<kCompactorFirst, 2>;
 
 struct Job {
-  int32_t l, h, K, first_moved;
+  int32_t l, h, K, first_moved, slot;
 };
 
 struct Smem {
@@ -89,20 +92,33 @@ struct Smem {
 };
 
 // GQA gives one ring stage (32 KB) to the per-head probability sum so that
-// segments up to ~8k tokens still fit the 227-KB SMEM plan.
-__host__ __device__ inline Smem plan(int bs, int max_T, int max_K, bool gqa = false) {
+// segments up to ~8k tokens still fit the 227-KB SMEM plan. Longer segments take
+// the spill variant: z_t / keys, the GQA sum and the kept-index hand-off live in a
+// per-CTA global row (spill_row_floats), the compactors read the block table in
+// place, and SMEM holds only the TMA ring, B and the barriers -- any T fits.
+__host__ __device__ inline Smem plan(int bs, int max_T, int max_K, bool gqa = false,
+                                     bool spill = false) {
   Smem p;
   p.max_nb = (max_T + bs - 1) / bs;
   p.max_K = max_K;
   p.off_ring = 0;
-  p.off_b = p.off_ring + ea_stages(gqa) * kStageBytes;
+  p.off_b = p.off_ring + ea_stages(gqa, spill) * kStageBytes;
   p.off_zt = p.off_b + 2 * kBBytes;
-  p.off_acc = p.off_zt + ((max_T * 4 + 15) & ~15);              // GQA: sum over heads of p_t
-  p.off_idx = p.off_acc + (gqa ? ((max_T * 4 + 15) & ~15) : 0);
-  p.off_ctab = p.off_idx + 2 * ((max_K * 4 + 15) & ~15);
-  p.off_bar = p.off_ctab + 2 * ((p.max_nb * 4 + 15) & ~15);
+  if (spill) {
+    p.off_acc = p.off_idx = p.off_ctab = p.off_bar = p.off_zt;
+  } else {
+    p.off_acc = p.off_zt + ((max_T * 4 + 15) & ~15);              // GQA: sum over heads of p_t
+    p.off_idx = p.off_acc + (gqa ? ((max_T * 4 + 15) & ~15) : 0);
+    p.off_ctab = p.off_idx + 2 * ((max_K * 4 + 15) & ~15);
+    p.off_bar = p.off_ctab + 2 * ((p.max_nb * 4 + 15) & ~15);
+  }
   p.total = p.off_bar + 64 * 8 + 1024;
   return p;
+}
+
+__host__ __device__ inline int64_t spill_row_floats(int max_T, int max_K, bool gqa) {
+  const int64_t tp = (max_T + 3) & ~3, kp = (max_K + 3) & ~3;
+  return tp * (gqa ? 2 : 1) + 2 * kp;
 }
 
 // Positions of one segment's stages in the global FIFO ring sequence:
@@ -146,13 +162,13 @@ using namespace ea;
 
 // T = __half or __nv_bfloat16: the K/V tiles' type; Sigma / mu are split into
 // hi + lo parts of the same type (fp16: ~22 significant bits, bf16: ~16).
-template <typename T, bool kGqa>
+template <typename T, bool kGqa, bool kSpill>
 __global__ void __launch_bounds__(kEaThreads, 1)
     ea_tc_kernel(char* __restrict__ arena, const int32_t* __restrict__ table, const Geom g,
                  const __grid_constant__ PressBatch b, const PressParams pp,
                  const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap cmap,
                  const float* __restrict__ mean_q, const fc_press_outputs out, int n_items,
-                 int max_K) {
+                 int max_K, float* __restrict__ spill) {
   extern __shared__ unsigned char smem_raw[];
   __shared__ SelectScratch ss;
   __shared__ uint32_t s_tmem;
@@ -161,17 +177,21 @@ __global__ void __launch_bounds__(kEaThreads, 1)
 
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  constexpr int kStages = ea_stages(kGqa);
-  const Smem P = plan(g.bs, b.max_T, max_K, kGqa);
+  constexpr int kStages = ea_stages(kGqa, kSpill);
+  const Smem P = plan(g.bs, b.max_T, max_K, kGqa, kSpill);
   const int gq = kGqa ? pp.num_q_heads / g.H : 1;
   unsigned char* ring = smem + P.off_ring;
   unsigned char* bmat = smem + P.off_b;  // [hi | lo]
-  float* zt = reinterpret_cast<float*>(smem + P.off_zt);
-  float* pacc = reinterpret_cast<float*>(smem + P.off_acc);   // valid when kGqa
   const int k_stride = ((max_K * 4 + 15) & ~15) / 4;
   const int nb_stride = ((P.max_nb * 4 + 15) & ~15) / 4;
-  int32_t* idxbuf = reinterpret_cast<int32_t*>(smem + P.off_idx);
-  int32_t* ctab = reinterpret_cast<int32_t*>(smem + P.off_ctab);
+  float* const row = kSpill ? spill + (int64_t)blockIdx.x * spill_row_floats(b.max_T, max_K, kGqa)
+                            : nullptr;
+  const int64_t t_pad = (b.max_T + 3) & ~3;
+  float* zt = kSpill ? row : reinterpret_cast<float*>(smem + P.off_zt);
+  float* pacc = kSpill ? row + t_pad : reinterpret_cast<float*>(smem + P.off_acc);   // kGqa
+  int32_t* idxbuf = kSpill ? reinterpret_cast<int32_t*>(row + t_pad * (kGqa ? 2 : 1))
+                           : reinterpret_cast<int32_t*>(smem + P.off_idx);
+  int32_t* ctab = reinterpret_cast<int32_t*>(smem + P.off_ctab);   // unused when kSpill
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.off_bar);
   uint64_t* st_full = bars;                  // [kStages]
   uint64_t* st_empty = bars + kStages;       // [kStages] 8 arrivals (consumer warps)
@@ -322,7 +342,8 @@ __global__ void __launch_bounds__(kEaThreads, 1)
       if (Compactors::tid() == 0) EA_STAMP(it, 6);
       const Job job = s_job[jb];
       char* seg = arena + g.seg_base(job.l, 0, job.h);
-      compact_rows<kD * 2, Compactors, FC_EA_CITEMS, FC_EA_CPF>(seg, g, ctab + jb * nb_stride, ctab + jb * nb_stride,
+      const int32_t* tab = kSpill ? table + (int64_t)job.slot * g.max_bpr : ctab + jb * nb_stride;
+      compact_rows<kD * 2, Compactors, FC_EA_CITEMS, FC_EA_CPF>(seg, g, tab, tab,
                                           idxbuf + jb * k_stride, job.K, job.first_moved);
       Compactors::sync();
       if (Compactors::tid() == 0) {
@@ -516,7 +537,8 @@ __global__ void __launch_bounds__(kEaThreads, 1)
       // ---- select into the hand-off buffer ----
       tc::mbar_wait(&job_empty[jb], ((it >> 1) & 1) ^ 1);
       int32_t* idx = idxbuf + jb * k_stride;
-      for (int i = ct; i < nb; i += kThreads) ctab[jb * nb_stride + i] = table[(int64_t)q.slot * g.max_bpr + i];
+      if (!kSpill)
+        for (int i = ct; i < nb; i += kThreads) ctab[jb * nb_stride + i] = table[(int64_t)q.slot * g.max_bpr + i];
       Consumers::sync();
       if (b.per_segment && q.seg0 < T_len) {
         select_emit<Consumers>(keys, q.seg0, q.K0, idx, 0, 0, ss);
@@ -528,7 +550,7 @@ __global__ void __launch_bounds__(kEaThreads, 1)
         int32_t* ko = out.kept_idx + q.kept_off + (int64_t)lh * K;
         for (int j = ct; j < K; j += kThreads) ko[j] = idx[j];
       }
-      if (ct == 0) s_job[jb] = Job{l, h, K, min(ss.first_drop, K)};
+      if (ct == 0) s_job[jb] = Job{l, h, K, min(ss.first_drop, K), q.slot};
       Consumers::sync();
       if (ct == 0) {
         EA_STAMP(it, 5);
@@ -554,14 +576,27 @@ bool ea_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T,
   if ((dtype != FC_F16 && dtype != FC_BF16) || g.D != kD) return false;
   if (pp.num_q_heads % g.H != 0 || pp.num_q_heads / g.H > 8) return false;   // GQA: gq <= 8
   if (g.bs < 8 || g.bs > 128) return false;
-  return plan(g.bs, max_T, max_K, pp.num_q_heads != g.H).total <= kDynSmemBudget;
+  (void)max_T;
+  (void)max_K;
+  return true;   // any T: segments beyond the SMEM plan take the spill variant
+}
+
+static bool ea_needs_spill(const Geom& g, int max_T, int max_K, bool gqa) {
+  return plan(g.bs, max_T, max_K, gqa).total > kDynSmemBudget;
+}
+
+int64_t ea_tc_workspace_floats(const Geom& g, int num_q_heads, int max_T, int max_K) {
+  const bool gqa = num_q_heads != g.H;
+  if (!ea_needs_spill(g, max_T, max_K, gqa)) return 0;
+  return (int64_t)sm_count() * spill_row_floats(max_T, max_K, gqa);
 }
 
 fc_status encode_rows(CUtensorMap* map, const void* base, int dtype, int D, uint64_t rows, int box_rows);
 
 fc_status launch_ea_tc(const Geom& g, int dtype, char* arena, const int32_t* table,
                        const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
-                       const fc_press_outputs& out, int max_K, cudaStream_t stream, bool dry_run) {
+                       const fc_press_outputs& out, int max_K, float* ws, int64_t ws_floats,
+                       cudaStream_t stream, bool dry_run) {
   CUtensorMap kmap, cmap;
   const uint64_t rows = (uint64_t)g.L * g.num_blocks * 2 * g.H * g.bs;
   fc_status st = encode_rows(&kmap, arena, dtype, g.D, rows, g.bs);
@@ -569,25 +604,35 @@ fc_status launch_ea_tc(const Geom& g, int dtype, char* arena, const int32_t* tab
   st = encode_rows(&cmap, in.cov_q, FC_F32, g.D, (uint64_t)b.n_total * g.L * pp.num_q_heads * g.D, 64);
   if (st != FC_OK) return st;
   const bool gqa = pp.num_q_heads != g.H;
-  const Smem P = plan(g.bs, b.max_T, max_K, gqa);
+  const bool spill = ea_needs_spill(g, b.max_T, max_K, gqa);
+  const Smem P = plan(g.bs, b.max_T, max_K, gqa, spill);
   if (P.total > kDynSmemBudget)
     return set_error(FC_ERR_UNSUPPORTED, "ExpectedAttention tensor-core plan exceeds the SMEM budget");
-  if (dry_run) return FC_OK;
+  if (dry_run) return FC_OK;   // the pool sizes the spill workspace next
   const int n_items = b.n * g.L * g.H;
   const int sms = sm_count();
-  const int grid = n_items < sms ? n_items : sms;
+  int grid = n_items < sms ? n_items : sms;
+  if (spill) {
+    const int64_t row = spill_row_floats(b.max_T, max_K, gqa);
+    if (ws_floats < row) return set_error(FC_ERR_INVALID_STATE, "EA spill workspace too small");
+    grid = (int)std::min<int64_t>(grid, ws_floats / row);
+  }
   auto launch = [&](auto kern) -> fc_status {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P.total);
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(ea_tc)");
     kern<<<grid, kEaThreads, P.total, stream>>>(arena, table, g, b, pp, kmap, cmap, in.mean_q, out,
-                                                n_items, max_K);
+                                                n_items, max_K, ws);
     note_launch();
     note_path(kPathTc);
     return cuda_check(cudaGetLastError(), "ea_tc_kernel");
   };
-  if (dtype == FC_BF16)
-    return gqa ? launch(ea_tc_kernel<__nv_bfloat16, true>) : launch(ea_tc_kernel<__nv_bfloat16, false>);
-  return gqa ? launch(ea_tc_kernel<__half, true>) : launch(ea_tc_kernel<__half, false>);
+  if (dtype == FC_BF16) {
+    if (spill)
+      return gqa ? launch(ea_tc_kernel<__nv_bfloat16, true, true>) : launch(ea_tc_kernel<__nv_bfloat16, false, true>);
+    return gqa ? launch(ea_tc_kernel<__nv_bfloat16, true, false>) : launch(ea_tc_kernel<__nv_bfloat16, false, false>);
+  }
+  if (spill) return gqa ? launch(ea_tc_kernel<__half, true, true>) : launch(ea_tc_kernel<__half, false, true>);
+  return gqa ? launch(ea_tc_kernel<__half, true, false>) : launch(ea_tc_kernel<__half, false, false>);
 }
 
 }  // namespace fc

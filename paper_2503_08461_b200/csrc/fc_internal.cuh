@@ -209,11 +209,17 @@ fc_status launch_press(const Geom& g, int dtype, char* arena, const int32_t* src
 bool snapkv_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T, int max_K);
 fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t* table,
                            const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
-                           const fc_press_outputs& out, cudaStream_t stream, bool dry_run);
+                           const fc_press_outputs& out, float* ws, int64_t ws_floats,
+                           cudaStream_t stream, bool dry_run);
+// spill rows of SnapKV tensor-core segments beyond its SMEM plan (0 if none)
+int64_t snapkv_tc_workspace_floats(const Geom& g, int max_T, int max_K);
 bool ea_tc_supported(const Geom& g, int dtype, const PressParams& pp, int max_T, int max_K);
 fc_status launch_ea_tc(const Geom& g, int dtype, char* arena, const int32_t* table,
                        const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
-                       const fc_press_outputs& out, int max_K, cudaStream_t stream, bool dry_run);
+                       const fc_press_outputs& out, int max_K, float* ws, int64_t ws_floats,
+                       cudaStream_t stream, bool dry_run);
+// spill rows of ExpectedAttention tensor-core segments beyond its SMEM plan (0 if none)
+int64_t ea_tc_workspace_floats(const Geom& g, int num_q_heads, int max_T, int max_K);
 int64_t press_workspace_floats(const Geom& g, int kind, int window, int num_q_heads, int max_T);
 
 // decode kernels (fc_decode.cu)

@@ -609,10 +609,13 @@ static bool needs_spill(const Geom& g, int kind, int window, int max_T, bool in_
 }
 
 int64_t press_workspace_floats(const Geom& g, int kind, int window, int num_q_heads, int max_T) {
-  (void)num_q_heads;
   int64_t n = snap_ws_floats(kind, window, max_T);
   if (needs_spill(g, kind, window, max_T, /*in_place=*/false))
     n += (int64_t)sm_count() * kSpillCtasPerSm * spill_floats(kind, max_T);
+  if (kind == FC_PRESS_EXPECTED_ATTENTION)   // the tensor-core kernels' spill rows (K <= T)
+    n = std::max(n, ea_tc_workspace_floats(g, num_q_heads, max_T, max_T));
+  if (kind == FC_PRESS_SNAPKV)
+    n = std::max(n, snapkv_tc_workspace_floats(g, max_T, max_T));
   return n;
 }
 
@@ -643,8 +646,10 @@ static fc_status launch_one(const Geom& g, char* arena, const int32_t* src, int3
     };
     auto run_tc = [&](const PressBatch& bb, int max_K) {
       return KIND == FC_PRESS_SNAPKV
-                 ? launch_snapkv_tc(g, Elem<T>::kDtype, arena, src, bb, pp, in, out, stream, dry)
-                 : launch_ea_tc(g, Elem<T>::kDtype, arena, src, bb, pp, in, out, max_K, stream, dry);
+                 ? launch_snapkv_tc(g, Elem<T>::kDtype, arena, src, bb, pp, in, out, ws, ws_floats,
+                                    stream, dry)
+                 : launch_ea_tc(g, Elem<T>::kDtype, arena, src, bb, pp, in, out, max_K, ws, ws_floats,
+                                stream, dry);
     };
     int max_K = 1;
     for (int i = 0; i < b.n; ++i) max_K = max_K > b.req[i].K ? max_K : b.req[i].K;

@@ -26,6 +26,7 @@
 // the reference ceil rule (kv.py:169-194).
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cstring>
 #include <mutex>
@@ -64,7 +65,7 @@ using Consumers = NamedGroup<kConsumerFirst, 1>;
 using Compactors = NamedGroup<kCompactorFirst, 2>;
 
 struct CompactJob {  // consumer -> compactor hand-off of one segment
-  int32_t l, h, K, first_moved;
+  int32_t l, h, K, first_moved, slot;
 };
 
 #ifndef FC_SNAP_ASYNC_COMPACT
@@ -88,7 +89,17 @@ struct TcSmem {
 
 __host__ __device__ inline int snap_k_stride(int max_K) { return ((max_K * 4 + 15) & ~15) / 4; }
 
-__host__ __device__ inline TcSmem tc_smem_plan(int D, int bs, int max_T, int max_K) {
+// spill: segments too long for the SMEM arrays keep the block tables in global memory
+// (read in place) and the T-sized arrays (scores / keys, window means, the kept-index
+// hand-off) in a per-CTA global row of snap_spill_floats(); SMEM then holds only the
+// TMA ring, the window queries, the barriers and the compaction ring.
+__host__ __device__ inline int64_t snap_spill_floats(int max_T, int max_K) {
+  const int64_t tp = (max_T + 3) & ~3;
+  return tp + (8 + tp) + 2 * snap_k_stride(max_K);
+}
+
+__host__ __device__ inline TcSmem tc_smem_plan(int D, int bs, int max_T, int max_K,
+                                               bool spill = false) {
   TcSmem p;
   p.tile_bytes = kTileM * D * 2;
   p.q_bytes = (kWin * D * 2 + 1023) & ~1023;
@@ -96,11 +107,15 @@ __host__ __device__ inline TcSmem tc_smem_plan(int D, int bs, int max_T, int max
   p.off_stage = 0;  // 1024-aligned base
   p.off_q = p.off_stage + kTcStages * p.tile_bytes;
   p.off_ptab = p.off_q + 2 * p.q_bytes;
-  p.off_ctab = p.off_ptab + ((p.max_nb * 4 + 15) & ~15);          // [2][max_nb]
-  p.off_idx = p.off_ctab + 2 * ((p.max_nb * 4 + 15) & ~15);        // [2][max_K] kept positions
-  p.off_sc = p.off_idx + 2 * snap_k_stride(max_K) * 4;
-  p.off_s1 = p.off_sc + ((max_T * 4 + 15) & ~15);                   // [8 zeros][max_T]
-  p.off_bar = p.off_s1 + (((max_T + 8) * 4 + 15) & ~15);
+  if (spill) {
+    p.off_ctab = p.off_idx = p.off_sc = p.off_s1 = p.off_bar = p.off_ptab;
+  } else {
+    p.off_ctab = p.off_ptab + ((p.max_nb * 4 + 15) & ~15);          // [2][max_nb]
+    p.off_idx = p.off_ctab + 2 * ((p.max_nb * 4 + 15) & ~15);        // [2][max_K] kept positions
+    p.off_sc = p.off_idx + 2 * snap_k_stride(max_K) * 4;
+    p.off_s1 = p.off_sc + ((max_T * 4 + 15) & ~15);                   // [8 zeros][max_T]
+    p.off_bar = p.off_s1 + (((max_T + 8) * 4 + 15) & ~15);
+  }
   p.off_cbuf = p.off_bar + (((2 * kTcStages + 8 + 2 * kSlots) * 8 + 127) & ~127);
   p.total = p.off_bar + (2 * kTcStages + 8 + 2 * kSlots) * 8 + 1024;
   // the compactors' cp.async ring (D * 2-byte rows, 4 x 32-rank chunks) when it fits
@@ -110,13 +125,13 @@ __host__ __device__ inline TcSmem tc_smem_plan(int D, int bs, int max_T, int max
   return p;
 }
 
-template <typename T, int D, bool kGqa>
+template <typename T, int D, bool kGqa, bool kSpill>
 __global__ void __launch_bounds__(kTcThreads, 1)
     snapkv_tc_kernel(char* __restrict__ arena, const int32_t* __restrict__ table, const Geom g,
                      const __grid_constant__ PressBatch b, const PressParams pp,
                      const __grid_constant__ CUtensorMap kmap,
                      const __grid_constant__ CUtensorMap qmap, const fc_press_outputs out,
-                     int n_items, int max_K) {
+                     int n_items, int max_K, float* __restrict__ spill) {
   constexpr int kHalves = D / 64;  // 128-byte K-dim slabs
   constexpr int kKSteps = D / 16;  // UMMA_K = 16 for 16-bit inputs
   constexpr int kFmt = Elem<T>::kDtype == FC_BF16 ? 1 : 0;
@@ -129,18 +144,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  const TcSmem plan = tc_smem_plan(D, g.bs, b.max_T, max_K);
+  const TcSmem plan = tc_smem_plan(D, g.bs, b.max_T, max_K, kSpill);
   unsigned char* stages = smem + plan.off_stage;
   unsigned char* qbuf = smem + plan.off_q;
-  int32_t* ptab = reinterpret_cast<int32_t*>(smem + plan.off_ptab);
+  int32_t* ptab = reinterpret_cast<int32_t*>(smem + plan.off_ptab);   // unused when kSpill
   const int nb_stride = ((plan.max_nb * 4 + 15) & ~15) / 4;
   const int k_stride = snap_k_stride(max_K);
   int32_t* ctab = reinterpret_cast<int32_t*>(smem + plan.off_ctab);   // [2][nb_stride]
-  int32_t* idxbuf = reinterpret_cast<int32_t*>(smem + plan.off_idx);  // [2][k_stride]
   __shared__ CompactJob s_job[2];
-  float* sc = reinterpret_cast<float*>(smem + plan.off_sc);
+  float* const row = kSpill ? spill + (int64_t)blockIdx.x * snap_spill_floats(b.max_T, max_K)
+                            : nullptr;
+  const int64_t t_pad = (b.max_T + 3) & ~3;
+  float* sc = kSpill ? row : reinterpret_cast<float*>(smem + plan.off_sc);
   // window means, front-padded with 8 zeros so the pooling window needs no bounds
-  float* s1 = reinterpret_cast<float*>(smem + plan.off_s1) + 8;
+  float* s1 = (kSpill ? row + t_pad : reinterpret_cast<float*>(smem + plan.off_s1)) + 8;
+  int32_t* idxbuf = kSpill ? reinterpret_cast<int32_t*>(row + t_pad + 8 + t_pad)
+                           : reinterpret_cast<int32_t*>(smem + plan.off_idx);  // [2][k_stride]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + plan.off_bar);
   uint64_t* st_full = bars;
   uint64_t* st_empty = bars + kTcStages;
@@ -175,8 +194,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int r = item / LH, lh = item % LH, l = lh / g.H, h = lh % g.H;
       const PressReq q = b.req[r];
       const int nb = (q.T + g.bs - 1) / g.bs, ntiles = (q.T + kTileM - 1) / kTileM;
+      const int32_t* btab = kSpill ? table + (int64_t)q.slot * g.max_bpr : ptab;
       __syncwarp();
-      for (int i = lane; i < nb; i += 32) ptab[i] = table[(int64_t)q.slot * g.max_bpr + i];
+      if (!kSpill)
+        for (int i = lane; i < nb; i += 32) ptab[i] = table[(int64_t)q.slot * g.max_bpr + i];
       __syncwarp();
       // GQA: the gq query heads sharing this kv head are scored one after the
       // other ("units"); the first gq - 1 passes over K ask L2 to keep the tiles
@@ -214,7 +235,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const bool reread = gi + 1 < gq || (nload > ntiles && kl < ntiles);
           const uint64_t pol = (FC_SNAP_L2HINT && reread) ? pol_last : pol_first;
           for (int c = lane; c < n_chunks; c += 32) {
-            const int64_t row0 = row_l + (int64_t)ptab[k * chunks + c] * 2 * g.H * g.bs;
+            const int64_t row0 = row_l + (int64_t)btab[k * chunks + c] * 2 * g.H * g.bs;
 #pragma unroll
             for (int hf = 0; hf < kHalves; ++hf) {
               if (FC_SNAP_L2HINT)
@@ -272,14 +293,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (Compactors::tid() == 0) FC_STAMP(it, 6);
       const CompactJob job = s_job[jb];
       char* seg = arena + g.seg_base(job.l, 0, job.h);
+      const int32_t* tab = kSpill ? table + (int64_t)job.slot * g.max_bpr : ctab + jb * nb_stride;
 #ifndef FC_NO_COMPACT
       if (plan.async_compact)
         compact_rows_async<D * (int)sizeof(T), Compactors, FC_SNAP_CRANKS, FC_SNAP_CBUFS>(
-            seg, g, ctab + jb * nb_stride, ctab + jb * nb_stride, idxbuf + jb * k_stride, job.K,
-            job.first_moved, smem + plan.off_cbuf);
+            seg, g, tab, tab, idxbuf + jb * k_stride, job.K, job.first_moved,
+            smem + plan.off_cbuf);
       else
-        compact_rows<D * (int)sizeof(T), Compactors, 8>(seg, g, ctab + jb * nb_stride,
-                                                     ctab + jb * nb_stride, idxbuf + jb * k_stride,
+        compact_rows<D * (int)sizeof(T), Compactors, 8>(seg, g, tab, tab, idxbuf + jb * k_stride,
                                                      job.K, job.first_moved);
 #endif
       Compactors::sync();
@@ -555,7 +576,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc::mbar_wait(&job_empty[jb], ((it >> 1) & 1) ^ 1);
       if (ct == 0) FC_STAMP(it, 13);
       int32_t* idx = idxbuf + jb * k_stride;
-      for (int i = ct; i < nb; i += kThreads) ctab[jb * nb_stride + i] = table[(int64_t)q.slot * g.max_bpr + i];
+      if (!kSpill)
+        for (int i = ct; i < nb; i += kThreads) ctab[jb * nb_stride + i] = table[(int64_t)q.slot * g.max_bpr + i];
       if (ct == 0) FC_STAMP(it, 14);
       if (b.per_segment && q.seg0 < T_len) {
         select_emit<Consumers>(keys, q.seg0, q.K0, idx, 0, 0, ss);
@@ -567,7 +589,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         int32_t* ko = out.kept_idx + q.kept_off + (int64_t)lh * K;
         for (int j = ct; j < K; j += kThreads) ko[j] = idx[j];
       }
-      if (ct == 0) s_job[jb] = CompactJob{l, h, K, min(ss.first_drop, K)};
+      if (ct == 0) s_job[jb] = CompactJob{l, h, K, min(ss.first_drop, K), q.slot};
       Consumers::sync();  // idx, ctab, job complete; sc / ss reused by the next segment
       if (ct == 0) {
         FC_STAMP(it, 5);
@@ -630,14 +652,25 @@ bool snapkv_tc_supported(const Geom& g, int dtype, const PressParams& pp, int ma
   if (pp.num_q_heads % g.H != 0 || pp.num_q_heads / g.H > 8) return false;   // GQA: gq <= 8
   if (pp.window != 32) return false;               // one 32x32b.x32 TMEM load per tile
   if (g.bs < 8 || g.bs > 128) return false;
-  // segments beyond the TMEM ring (T > kSlots * 128) take the two-pass path
-  if (tc_smem_plan(g.D, g.bs, max_T, max_K).total > kDynSmemBudget) return false;
+  // segments beyond the TMEM ring (T > kSlots * 128) take the two-pass path, beyond the
+  // SMEM arrays the spill variant: any T runs on the tensor cores
+  (void)max_T;
+  (void)max_K;
   return true;
+}
+
+static bool snap_needs_spill(const Geom& g, int max_T, int max_K) {
+  return tc_smem_plan(g.D, g.bs, max_T, max_K).total > kDynSmemBudget;
+}
+
+int64_t snapkv_tc_workspace_floats(const Geom& g, int max_T, int max_K) {
+  return snap_needs_spill(g, max_T, max_K) ? (int64_t)sm_count() * snap_spill_floats(max_T, max_K) : 0;
 }
 
 fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t* table,
                            const PressBatch& b, const PressParams& pp, const fc_press_inputs& in,
-                           const fc_press_outputs& out, cudaStream_t stream, bool dry_run) {
+                           const fc_press_outputs& out, float* ws, int64_t ws_floats,
+                           cudaStream_t stream, bool dry_run) {
   const int n_requests_total = b.n_total;
   CUtensorMap kmap, qmap;
   const uint64_t rows = (uint64_t)g.L * g.num_blocks * 2 * g.H * g.bs;
@@ -648,30 +681,40 @@ fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t*
   if (st != FC_OK) return st;
   int max_K = 1;
   for (int i = 0; i < b.n; ++i) max_K = max_K > b.req[i].K ? max_K : b.req[i].K;
-  const TcSmem plan = tc_smem_plan(g.D, g.bs, b.max_T, max_K);
+  const bool spill = snap_needs_spill(g, b.max_T, max_K);
+  const TcSmem plan = tc_smem_plan(g.D, g.bs, b.max_T, max_K, spill);
   if (plan.total > kDynSmemBudget)
     return set_error(FC_ERR_UNSUPPORTED, "SnapKV tensor-core plan exceeds the SMEM budget");
-  if (dry_run) return FC_OK;
+  if (dry_run) return FC_OK;   // the pool sizes the spill workspace next
   const int n_items = b.n * g.L * g.H;
   const int sms = sm_count();
-  const int grid = n_items < sms ? n_items : sms;
+  int grid = n_items < sms ? n_items : sms;
+  if (spill) {
+    const int64_t row = snap_spill_floats(b.max_T, max_K);
+    if (ws_floats < row) return set_error(FC_ERR_INVALID_STATE, "SnapKV spill workspace too small");
+    grid = (int)std::min<int64_t>(grid, ws_floats / row);
+  }
   auto launch = [&](auto kern) -> fc_status {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.total);
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(snapkv_tc)");
     kern<<<grid, kTcThreads, plan.total, stream>>>(arena, table, g, b, pp, kmap, qmap, out, n_items,
-                                                   max_K);
+                                                   max_K, ws);
     note_launch();
     note_path(kPathTc);
     return cuda_check(cudaGetLastError(), "snapkv_tc_kernel");
   };
   // g = 1 gets its own instantiation (the unit loop folds away)
   const bool gqa = pp.num_q_heads != g.H;
-  if (dtype == FC_BF16) {
-    if (g.D == 64) return gqa ? launch(snapkv_tc_kernel<__nv_bfloat16, 64, true>) : launch(snapkv_tc_kernel<__nv_bfloat16, 64, false>);
-    return gqa ? launch(snapkv_tc_kernel<__nv_bfloat16, 128, true>) : launch(snapkv_tc_kernel<__nv_bfloat16, 128, false>);
-  }
-  if (g.D == 64) return gqa ? launch(snapkv_tc_kernel<__half, 64, true>) : launch(snapkv_tc_kernel<__half, 64, false>);
-  return gqa ? launch(snapkv_tc_kernel<__half, 128, true>) : launch(snapkv_tc_kernel<__half, 128, false>);
+  auto pick = [&](auto tag) -> fc_status {
+    using T = decltype(tag);
+    if (g.D == 64) {
+      if (spill) return gqa ? launch(snapkv_tc_kernel<T, 64, true, true>) : launch(snapkv_tc_kernel<T, 64, false, true>);
+      return gqa ? launch(snapkv_tc_kernel<T, 64, true, false>) : launch(snapkv_tc_kernel<T, 64, false, false>);
+    }
+    if (spill) return gqa ? launch(snapkv_tc_kernel<T, 128, true, true>) : launch(snapkv_tc_kernel<T, 128, false, true>);
+    return gqa ? launch(snapkv_tc_kernel<T, 128, true, false>) : launch(snapkv_tc_kernel<T, 128, false, false>);
+  };
+  return dtype == FC_BF16 ? pick(__nv_bfloat16()) : pick(__half());
 }
 
 }  // namespace fc

@@ -168,12 +168,13 @@ def test_press_refusals_leave_the_batch_untouched(cuda):
 
 
 @pytest.mark.parametrize("gq,specs", [
-    (1, [(0, 9000), (576, 500), (3, 1200)]),     # 9000 tokens exceed the EA tensor-core SMEM plan
-    (4, [(576, 6000), (0, 300), (17, 900)]),     # GQA: the per-head sum array leaves room for ~5k
+    (1, [(0, 9000), (576, 500), (3, 1200)]),     # 9000 tokens: the tensor-core kernel's spill variant
+    (4, [(576, 6000), (0, 300), (17, 900)]),     # GQA: the per-head sum array spills past ~5k tokens
 ])
 def test_expected_attention_mixed_fit_batches(cuda, gq, specs):
-    """Requests that fit the tensor-core kernel run there, the rest on the SIMT kernel, in one
-    compress call; every score matches the oracle either way."""
+    """Short and long requests in one compress call: the batch's longest request puts it on
+    the tensor-core kernel's spill variant (SMEM arrays in a global row); every score
+    matches the oracle."""
     cfg = ModelConfig("m", 1, 2, 128, 2)
     pool = KVCachePool(cfg, (1 << 16) * cfg.bytes_per_token, device=cuda, kv_dtype="float16",
                        max_handles=16, max_tokens_per_handle=16384, num_q_heads=2 * gq)
