@@ -54,6 +54,9 @@ CONFIGS = {
            "wave of config 4)",
     "c4": "ExpectedAttention at 25% keep on 256 mixed-length requests (1k-8k tokens) with pool "
           "alloc/free churn (admission waves, 140 GB pool) and fragmentation accounting",
+    "c2m": "LLaVA-1.5-7B-shaped KV (32 layers, 32 heads, d=128, 576 image + 512 text tokens) "
+           "batch 32 through the reference's own compressor (compress_tensor MEAN_POOL, factor 5, "
+           "kv.py:211-239) folded into the pool blocks (K7, SURVEY.md §8(f) row 1), fp16",
     "c2d": "decode after compression: config 2's batch (32 x 1088 tokens, Knorm 50% -> 544) "
            "then 64 decode steps, each = append one token per request + per layer write K/V and "
            "paged attention over the compacted blocks (SURVEY.md §8(f) row 2)",
@@ -71,7 +74,13 @@ Q_HEADS = {"c3g": 32, "c4g": 32}   # query heads when they differ from the kv he
 def workload(name: str):
     import numpy as np
 
-    from paper_2503_08461_b200 import CompressorSpec, ModelConfig, PressKind, split_modalities
+    from paper_2503_08461_b200 import (
+        CompressorSpec,
+        MapKind,
+        ModelConfig,
+        PressKind,
+        split_modalities,
+    )
 
     if name == "c1":
         cfg = ModelConfig("tiny", 4, 8, 64, 4)
@@ -81,6 +90,10 @@ def workload(name: str):
         cfg = ModelConfig("llava-7b", 32, 32, 128, 2)
         specs = [split_modalities(576, 512)] * 32
         return cfg, "float16", specs, CompressorSpec(factor=2, press=PressKind.KNORM)
+    if name == "c2m":
+        cfg = ModelConfig("llava-7b", 32, 32, 128, 2)
+        specs = [split_modalities(576, 512)] * 32
+        return cfg, "float16", specs, CompressorSpec(factor=5, map_kind=MapKind.MEAN_POOL)
     if name == "c3":
         cfg = ModelConfig("llava-7b", 32, 32, 128, 2)
         txt = np.random.default_rng(0).integers(64, 961, 64)
@@ -656,7 +669,8 @@ def press_leg(args, name, rank, world, local_rank, with_e2e):
     peak, peak_kind = measured_peak()
     press_avg = statistics.mean(press_ms)
     achieved = abytes / (press_avg / 1e3) / 1e9
-    kernel = {"knorm": "press_kernel<KNORM> (score + top-k + in-place compaction)",
+    kernel = {"chunk": "chunk_pool_kernel (reference compress_tensor fold into the blocks)",
+              "knorm": "press_kernel<KNORM> (score + top-k + in-place compaction)",
               "snapkv": "snapkv_tc_kernel (tcgen05 window QK^T + softmax/pool + top-k + compaction)",
               "expected_attention": "ea_tc_kernel (tcgen05 K.[Sigma;mu] + softmax*|V| + top-k + "
                                     "compaction)"}.get(comp.press.value, "press kernel")
@@ -720,9 +734,11 @@ def sampled_parity(pool, fill, specs, comp, ins, dtype, rids, n_segments, device
     import torch
 
     from oracle import parity
+    from paper_2503_08461_b200 import PressKind
 
     hs = fill()
-    res = pool.compress_batch(hs, comp, 1.0, return_indices=True, return_scores=True, **ins)
+    want = comp.press is not PressKind.CHUNK      # the chunk fold has no scores / indices
+    res = pool.compress_batch(hs, comp, 1.0, return_indices=want, return_scores=want, **ins)
     t0 = time.perf_counter()
     rep = parity.check_batch(pool, hs, specs, comp, res, dtype=dtype, seed=SYNTH_SEED, keys=rids,
                              inputs=ins, n_segments=n_segments)

@@ -20,13 +20,18 @@ the bars of SURVEY.md §8(c) / the BASELINE.json north star:
 * kept indices: Knorm exactly ``press.select``; SnapKV / EA the oracle set up to
   tolerated boundary swaps (``press.kept_set_mismatch``);
 * compacted payload: the K and V rows now stored at ranks 0..K_r-1 are bit copies of
-  the regenerated raw rows the GPU selected.
+  the regenerated raw rows the GPU selected;
+* the reference chunk compressor (MEAN_POOL / SEEDED_LINEAR folded into the pool): the
+  stored rows equal ``chunk.compress_tensor`` of each modality segment (pinned to the
+  reference's own golden vectors) -- bit-exact for MEAN_POOL on fp16/fp32, within 1e-2
+  (bf16) / 1e-6 (fp32) for SEEDED_LINEAR, whose reference output is float64.
 """
 
 from __future__ import annotations
 
 import numpy as np
 
+from . import chunk as ochunk
 from . import press as opress
 from . import synth as osynth
 
@@ -48,6 +53,41 @@ def sample_segments(lengths, num_layers: int, num_heads: int, n: int, seed: int 
             seen.add(t)
             picks.append(t)
     return picks
+
+
+def _stored_rows(pool, handle, layer, head, n):
+    """Ranks 0..n-1 of (layer, head) straight from the paged layer view: [2, n, D]."""
+    import torch
+
+    cache = pool.kv_cache(layer)                   # [NB, 2, H, bs, D]
+    bs = cache.shape[3]
+    j = torch.arange(n, device=cache.device)
+    seg = cache[handle.block_table.long()[j // bs], :, head, j % bs].transpose(0, 1).contiguous()
+    if seg.dtype == torch.bfloat16:
+        seg = seg.view(torch.int16)
+    return seg.cpu().numpy()
+
+
+def _check_chunk_rows(pool, handle, layer, head, k_st, v_st, seg_tokens, comp, dtype):
+    kind = comp.map_kind.value
+    got = _stored_rows(pool, handle, layer, head, opress.kept_budget(seg_tokens, comp.factor))
+    for kv, raw in ((0, k_st), (1, v_st)):
+        src = osynth.to_f32(raw, dtype) if dtype == "bfloat16" else raw
+        parts, start = [], 0
+        for n in (x for x in seg_tokens if x > 0):
+            parts.append(ochunk.compress_tensor(src[start:start + n], comp.factor, kind, comp.seed))
+            start += n
+        want = np.concatenate(parts)
+        if kind == "meanpool" and dtype != "bfloat16":
+            if not np.array_equal(got[kv].view(np.uint8), want.astype(raw.dtype).view(np.uint8)):
+                return f"{'KV'[kv]} rows differ from compress_tensor"
+        else:
+            g32 = osynth.to_f32(got[kv], dtype)
+            w32 = osynth.to_f32(osynth.cast_dtype(want.astype(np.float32), dtype), dtype)
+            tol = 1e-6 if dtype == "float32" else 1e-2
+            if not np.allclose(g32, w32, rtol=tol, atol=1e-6):
+                return f"{'KV'[kv]} rows beyond {tol} of compress_tensor"
+    return None
 
 
 def check_batch(pool, handles, raw_specs, comp, result, *, dtype: str, seed: int, keys,
@@ -72,6 +112,7 @@ def check_batch(pool, handles, raw_specs, comp, result, *, dtype: str, seed: int
     inputs = inputs or {}
     lengths = [s.total_tokens for s in raw_specs]
     picks = sample_segments(lengths, L, H, n_segments, sample_seed)
+    chunk_kind = comp.press is PressKind.CHUNK
     by_req: dict[int, list] = {}
     for r, layer, head in picks:
         by_req.setdefault(r, []).append((layer, head))
@@ -82,13 +123,19 @@ def check_batch(pool, handles, raw_specs, comp, result, *, dtype: str, seed: int
         t_len = spec.total_tokens
         seg_tokens = [s.token_count for s in spec.segments]
         k_r = opress.kept_budget(seg_tokens, comp.factor)
-        scores_r = result.scores[r]
-        kept_r = result.kept_idx[r]
+        scores_r = None if chunk_kind else result.scores[r]
+        kept_r = None if chunk_kind else result.kept_idx[r]
         for layer, head in segs:
             tag = f"req {r} layer {layer} head {head}"
             k_st = osynth.head_values(seed, keys[r], layer, 0, head, t_len, D, dtype, dist)
             v_st = osynth.head_values(seed, keys[r], layer, 1, head, t_len, D, dtype, dist)
             k32, v32 = osynth.to_f32(k_st, dtype), osynth.to_f32(v_st, dtype)
+            if chunk_kind:
+                why = _check_chunk_rows(pool, handles[r], layer, head, k_st, v_st, seg_tokens,
+                                        comp, dtype)
+                if why:
+                    failures.append(f"{tag}: {why}")
+                continue
             got_s = scores_r[layer, head].cpu().numpy()
             got_k = kept_r[layer, head].cpu().numpy().astype(np.int64)
             if comp.press is PressKind.KNORM:

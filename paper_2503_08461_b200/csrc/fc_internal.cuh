@@ -173,6 +173,15 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
                : "l"(p));
   return r;
 }
+// Same load without `volatile`: the compiler may batch several of them ahead of their
+// uses (only for data this kernel does not rewrite before reading it).
+__device__ __forceinline__ uint4 ld_stream_nv(const void* p) {
+  uint4 r;
+  asm("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
+}
 __device__ __forceinline__ void st_stream(void* p, const uint4& v) {
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w)

@@ -505,8 +505,11 @@ __global__ void __launch_bounds__(kThreads, KIND == FC_PRESS_KNORM ? FC_KN_MINB 
 // row count, cast to the pool dtype (numpy mean semantics, kv.py:227-231);
 // SEEDED_LINEAR: fp64 weighted sum with the renormalised weights, rounded to
 // the pool dtype (the reference returns fp64; the pool stores its dtype).
-template <typename T, int D>
-__global__ void __launch_bounds__(kThreads)
+#ifndef FC_CHUNK_MINB   // chunk-fold CTAs per SM the register budget is sized for
+#define FC_CHUNK_MINB 4
+#endif
+template <typename T, int D, bool kSeeded>
+__global__ void __launch_bounds__(kThreads, kSeeded ? 2 : FC_CHUNK_MINB)
     chunk_pool_kernel(char* __restrict__ arena, const int32_t* __restrict__ src_table,
                       const int32_t* __restrict__ dst_table, const Geom g,
                       const __grid_constant__ PressBatch b, const PressParams pp) {
@@ -533,48 +536,73 @@ __global__ void __launch_bounds__(kThreads)
   const int seg0 = q.seg0, K0 = q.K0;
   for (int j0 = 0; j0 < q.K; j0 += kChunk) {
     uint4 res[kItems];
+    // per item: source base row, row count m, and the byte offset of its vector
+    int s_first[kItems], m_rows[kItems];
+    int64_t voff[kItems];
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
       const int item = it * kThreads + threadIdx.x;
       const int row = item / (2 * kVecs), rem = item % (2 * kVecs);
       const int kv = rem / kVecs, vec = rem % kVecs;
       const int j = j0 + row;
-      if (j >= q.K) continue;
-      // segment of output row j
-      const bool second = j >= K0;
+      const bool second = j >= K0;   // output row j's modality segment
       const int sb = second ? seg0 : 0, ob = second ? K0 : 0, se = second ? q.T : seg0;
-      const int s_first = sb + (j - ob) * k;
-      const int m = min(k, se - s_first);
-      float accf[kEPV];
-      double accd[kEPV];
+      s_first[it] = sb + (j - ob) * k;
+      m_rows[it] = j < q.K ? min(k, se - s_first[it]) : 0;
+      voff[it] = kv * kv_off + vec * 16;
+    }
+    float accf[kItems][kEPV];
+    double accd[kSeeded ? kItems : 1][kEPV];
+#pragma unroll
+    for (int it = 0; it < kItems; ++it)
 #pragma unroll
       for (int e = 0; e < kEPV; ++e) {
-        accf[e] = 0.f;
-        accd[e] = 0.0;
+        accf[it][e] = 0.f;
+        if (kSeeded) accd[it][e] = 0.0;
       }
-      const double* w = pp.w_table + (int64_t)(m - 1) * k;
-      for (int i = 0; i < m; ++i) {
-        const int src = s_first + i;
-        float x[kEPV];
-        unpack16<T>(ld_stream(seg + kv * kv_off + (int64_t)s_src[src >> g.bs_shift] * g.block_stride +
-                              (int64_t)(src & (g.bs - 1)) * g.row_bytes + vec * 16),
-                    x);
-        if (pp.kind == FC_PRESS_MEANPOOL) {
+    // row i of every item's chunk is loaded together (kItems independent 16-B loads in
+    // flight per thread), then folded in the reference order: the accumulation chain is
+    // per item, so only the HBM latency of one row step is exposed per i
+    auto fold = [&](int it, int i, const uint4& raw) {
+      float x[kEPV];
+      unpack16<T>(raw, x);
+      if (!kSeeded) {
 #pragma unroll
-          for (int e = 0; e < kEPV; ++e) accf[e] = (i == 0) ? x[e] : __fadd_rn(accf[e], x[e]);
-        } else {
-          const double wi = w[i];
+        for (int e = 0; e < kEPV; ++e) accf[it][e] = (i == 0) ? x[e] : __fadd_rn(accf[it][e], x[e]);
+      } else {
+        const double wi = pp.w_table[(int64_t)(m_rows[it] - 1) * k + i];
 #pragma unroll
-          for (int e = 0; e < kEPV; ++e) accd[e] = fma(wi, (double)x[e], accd[e]);
-        }
+        for (int e = 0; e < kEPV; ++e) accd[it][e] = fma(wi, (double)x[e], accd[it][e]);
       }
+    };
+    auto load = [&](int it, int i) {
+      const int src = s_first[it] + i;
+      return ld_stream_nv(seg + voff[it] + (int64_t)s_src[src >> g.bs_shift] * g.block_stride +
+                          (int64_t)(src & (g.bs - 1)) * g.row_bytes);
+    };
+    // row i of every item's chunk is loaded together (kItems independent 16-B loads in
+    // flight per thread), then folded in the reference's sequential row order. (Two rows
+    // per step was measured slower: 5.20 vs 4.52 ms at c2m, the extra registers cost a
+    // CTA per SM.)
+    for (int i = 0; i < k; ++i) {
+      uint4 v[kItems];
+#pragma unroll
+      for (int it = 0; it < kItems; ++it)
+        if (i < m_rows[it]) v[it] = load(it, i);
+#pragma unroll
+      for (int it = 0; it < kItems; ++it)
+        if (i < m_rows[it]) fold(it, i, v[it]);
+    }
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
       T o[kEPV];
+      const int m = max(m_rows[it], 1);
 #pragma unroll
       for (int e = 0; e < kEPV; ++e) {
-        if (pp.kind == FC_PRESS_MEANPOOL)
-          o[e] = Elem<T>::from_f(__fdiv_rn(accf[e], (float)m));
+        if (!kSeeded)
+          o[e] = Elem<T>::from_f(__fdiv_rn(accf[it][e], (float)m));
         else
-          o[e] = Elem<T>::from_f((float)accd[e]);
+          o[e] = Elem<T>::from_f((float)accd[it][e]);
       }
       res[it] = *reinterpret_cast<uint4*>(o);
     }
@@ -631,7 +659,8 @@ static fc_status launch_one(const Geom& g, char* arena, const int32_t* src, int3
     if (smem > kDynSmemBudget)
       return set_error(FC_ERR_UNSUPPORTED, "request of %d tokens exceeds the chunk-fold SMEM plan", b.max_T);
     if (dry) return FC_OK;
-    auto kern = chunk_pool_kernel<T, D>;
+    auto kern = pp.kind == FC_PRESS_SEEDEDLINEAR ? chunk_pool_kernel<T, D, true>
+                                                 : chunk_pool_kernel<T, D, false>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<n_items, kThreads, smem, stream>>>(arena, src, dst, g, b, pp);

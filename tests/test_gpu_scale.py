@@ -1,7 +1,8 @@
 """Parity at BASELINE scale (run with -m gpu).
 
 The other GPU tests use small L/H so the whole batch can be re-scored on the CPU. Here
-the batches are the measured configurations themselves -- c2 (32 x 1088 tokens, Knorm),
+the batches are the measured configurations themselves -- c2 (32 x 1088 tokens, Knorm;
+and c2m, the same batch through the reference's mean-pool compressor folded in place),
 c3 (64 varlen requests, L=32, H=32, SnapKV on the persistent tcgen05 kernel) and one
 c4w admission wave (64 requests of 1k-8k tokens, ExpectedAttention on tcgen05) -- and the
 check is oracle/parity.check_batch on 64 sampled (request, layer, head) segments each:
@@ -27,7 +28,8 @@ import bench  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name,tc", [("c2", False), ("c3", True), ("c4w", True), ("c3g", True)])
+@pytest.mark.parametrize("name,tc", [("c2", False), ("c2m", False), ("c3", True), ("c4w", True),
+                                     ("c3g", True)])
 def test_full_batch_sampled_parity(cuda, name, tc):
     cfg, dtype, specs, comp = bench.workload(name)
     hq = bench.Q_HEADS.get(name, cfg.num_kv_heads)
@@ -44,9 +46,14 @@ def test_full_batch_sampled_parity(cuda, name, tc):
     rids = list(range(len(specs)))
     hs = pool.allocate_batch(rids, specs, 0.0)
     pool.synth_fill(hs, seed=bench.SYNTH_SEED)
-    res = pool.compress_batch(hs, comp, 1.0, return_indices=True, return_scores=True, **ins)
+    chunk = name == "c2m"        # the reference fold: no scores / indices
+    res = pool.compress_batch(hs, comp, 1.0, return_indices=not chunk, return_scores=not chunk,
+                              **ins)
     paths = pool.last_paths()
-    assert (paths["tc"] >= 1) == tc and (paths["simt"] == 0) == tc, paths
+    if chunk:
+        assert paths == {"tc": 0, "simt": 0, "chunk": 1}, paths
+    else:
+        assert (paths["tc"] >= 1) == tc and (paths["simt"] == 0) == tc, paths
     rep = parity.check_batch(pool, hs, specs, comp, res, dtype=dtype, seed=bench.SYNTH_SEED,
                              keys=rids, inputs=ins, n_segments=64)
     assert rep["segments"] >= 64 and rep["mismatches"] == 0, rep["failures"]
