@@ -2,6 +2,9 @@
 """Summarise an ncu --set full capture into profiles/ncu_<config>.json (+ a text digest).
 
     python scripts/ncu_summary.py gpurun_out/prof_c2.ncu-rep c2 [alg_bytes_per_launch]
+
+The first argument may also be the `ncu -i <rep> --page raw --csv` export of the report
+(a .csv file), which is what the GPU box sends back when the reports are too large.
 """
 import csv
 import io
@@ -24,8 +27,12 @@ KEYS = [
 def main():
     rep, config = sys.argv[1], sys.argv[2]
     alg = float(sys.argv[3]) if len(sys.argv) > 3 else None
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if rep.endswith(".csv"):
+        with open(rep) as f:
+            raw = f.read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     out = {"report": rep, "kernels": []}
