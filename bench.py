@@ -596,7 +596,8 @@ def run_ours(args, rank, world, local_rank):
             leg = press_leg(args, name, rank, world, local_rank, with_e2e=False)
             result["legs"][name] = {k: leg[k] for k in (
                 "value", "unit", "ms_per_step", "scaling", "dtype", "config", "hbm_gbs_per_gpu",
-                "kept_tokens_per_s", "roofline", "gpu_launches", "clocks", "parity", "paths")}
+                "kept_tokens_per_s", "roofline", "gpu_launches", "clocks", "parity", "paths")
+                if k in leg}
     return result
 
 

@@ -8,7 +8,7 @@ for c in c2 c3 c4w c2m c3l; do
   timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:"press_kernel|snapkv_tc|ea_tc|chunk_pool" -s 3 -c 1 \
     -o /tmp/prof_r02_$c -f python bench.py --config $c --steps 1 --warmup 3 --e2e-steps 0 \
-    --no-cpu-baseline --parity-segments 0 > gpurun_out/ncu_r02_$c.log 2>&1
+    --no-cpu-baseline --parity-segments 0 --legs "" > gpurun_out/ncu_r02_$c.log 2>&1
   tail -1 gpurun_out/ncu_r02_$c.log
   ncu -i /tmp/prof_r02_$c.ncu-rep --page raw --csv > gpurun_out/prof_r02_$c.raw.csv 2>/dev/null
   python scripts/ncu_lines.py /tmp/prof_r02_$c.ncu-rep 25 > gpurun_out/prof_r02_${c}_lines.txt 2>&1
