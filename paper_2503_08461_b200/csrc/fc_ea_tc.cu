@@ -540,12 +540,7 @@ __global__ void __launch_bounds__(kEaThreads, 1)
       if (!kSpill)
         for (int i = ct; i < nb; i += kThreads) ctab[jb * nb_stride + i] = table[(int64_t)q.slot * g.max_bpr + i];
       Consumers::sync();
-      if (b.per_segment && q.seg0 < T_len) {
-        select_emit<Consumers>(keys, q.seg0, q.K0, idx, 0, 0, ss);
-        select_emit<Consumers>(keys + q.seg0, T_len - q.seg0, K - q.K0, idx, q.K0, q.seg0, ss);
-      } else {
-        select_emit<Consumers>(keys, T_len, K, idx, 0, 0, ss);
-      }
+      select_request<Consumers>(keys, T_len, K, q.seg0, q.K0, b.per_segment, idx, ss);
       if (out.kept_idx) {
         int32_t* ko = out.kept_idx + q.kept_off + (int64_t)lh * K;
         for (int j = ct; j < K; j += kThreads) ko[j] = idx[j];

@@ -475,12 +475,7 @@ __global__ void __launch_bounds__(kThreads, KIND == FC_PRESS_KNORM ? FC_KN_MINB 
 
     // ---- phase 2: select (kept positions overwrite the keys, ascending) ----
     int32_t* idx = reinterpret_cast<int32_t*>(sc);
-    if (b.per_segment && q.seg0 < T_len) {
-      select_emit(keys, q.seg0, q.K0, idx, 0, 0, ss);
-      select_emit(keys + q.seg0, T_len - q.seg0, K - q.K0, idx, q.K0, q.seg0, ss);
-    } else {
-      select_emit(keys, T_len, K, idx, 0, 0, ss);
-    }
+    select_request(keys, T_len, K, q.seg0, q.K0, b.per_segment, idx, ss);
     if (out.kept_idx) {
       int32_t* ko = out.kept_idx + q.kept_off + (int64_t)lh * K;
       for (int j = threadIdx.x; j < K; j += kThreads) ko[j] = idx[j];

@@ -580,10 +580,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int i = ct; i < nb; i += kThreads) ctab[jb * nb_stride + i] = table[(int64_t)q.slot * g.max_bpr + i];
       if (ct == 0) FC_STAMP(it, 14);
       if (b.per_segment && q.seg0 < T_len) {
-        select_emit<Consumers>(keys, q.seg0, q.K0, idx, 0, 0, ss);
-        select_emit<Consumers>(keys + q.seg0, T_len - q.seg0, K - q.K0, idx, q.K0, q.seg0, ss);
+        select_emit<Consumers, kSpill>(keys, q.seg0, q.K0, idx, 0, 0, ss);
+        select_emit<Consumers, kSpill>(keys + q.seg0, T_len - q.seg0, K - q.K0, idx, q.K0, q.seg0, ss);
       } else {
-        select_emit<Consumers>(keys, T_len, K, idx, 0, 0, ss);
+        select_emit<Consumers, kSpill>(keys, T_len, K, idx, 0, 0, ss);
       }
       if (out.kept_idx) {
         int32_t* ko = out.kept_idx + q.kept_off + (int64_t)lh * K;
