@@ -57,6 +57,16 @@ __device__ __forceinline__ void trace_stamp(int it, int slot) {
 constexpr int kTcStages = FC_SNAP_STAGES;
 constexpr int kTileM = 128;
 constexpr int kSlots = 16;                      // TMEM ring: 16 x 32 fp32 columns
+#ifndef FC_SNAP_RESIDENT
+#define FC_SNAP_RESIDENT (kSlots - 2)
+#endif
+// A segment longer than the ring (ntiles > kSlots) is streamed in two passes; the
+// last kResident tiles of pass A stay in TMEM for pass B, which re-streams only the
+// first ntiles - kResident (two slots stay free so the re-stream starts at once).
+constexpr int kResident = FC_SNAP_RESIDENT;
+__host__ __device__ __forceinline__ int snap_loads(int ntiles) {
+  return ntiles > kSlots ? 2 * ntiles - kResident : ntiles;
+}
 constexpr int kWin = 32;                        // window queries (UMMA N)
 constexpr int kConsumerFirst = 64;              // warps 0,1 = producer, MMA
 constexpr int kCompactorFirst = kConsumerFirst + kThreads;
@@ -204,9 +214,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // so the repeats come from L2, not HBM.
       const int gq = kGqa ? pp.num_q_heads / g.H : 1;
       const int64_t row_l = (int64_t)l * g.num_blocks * 2 * g.H * g.bs + (int64_t)h * g.bs;
-      // a segment longer than the TMEM ring (T > kSlots * 128) is streamed twice:
-      // pass A (softmax statistics) and pass B (normalised window mean)
-      const int nload = ntiles > kSlots ? 2 * ntiles : ntiles;
+      // a segment longer than the TMEM ring (T > kSlots * 128) is streamed in two
+      // passes: pass A (softmax statistics) over every tile, pass B (normalised
+      // window mean) re-streams tiles [0, ntiles - kResident) only
+      const int nload = snap_loads(ntiles);
       for (int gi = 0; gi < gq; ++gi, ++unit) {
         if (lane == 0) {
           const int qb = unit & 1;
@@ -232,7 +243,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           unsigned char* dst = stages + st * plan.tile_bytes;
           // evict-last while a later pass (pass B, or the next query head) re-reads
           // the tile; evict-first on its last read
-          const bool reread = gi + 1 < gq || (nload > ntiles && kl < ntiles);
+          const bool reread = gi + 1 < gq || (nload > ntiles && kl < ntiles - kResident);
           const uint64_t pol = (FC_SNAP_L2HINT && reread) ? pol_last : pol_first;
           for (int c = lane; c < n_chunks; c += 32) {
             const int64_t row0 = row_l + (int64_t)btab[k * chunks + c] * 2 * g.H * g.bs;
@@ -262,7 +273,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int qb = unit & 1;
         tc::mbar_wait(&q_full[qb], (unit >> 1) & 1);
         const uint32_t q_base = tc::smem_u32(qbuf + qb * plan.q_bytes);
-        const int nload = ntiles > kSlots ? 2 * ntiles : ntiles;
+        const int nload = snap_loads(ntiles);
         for (int k = 0; k < nload; ++k, ++gtile) {
           const int st = gtile % kTcStages, sl = gtile % kSlots;
           tc::mbar_wait(&sl_empty[sl], ((gtile / kSlots) & 1) ^ 1);
@@ -454,9 +465,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc::fence_after_sync();
             float v[16];
             tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
-            tc::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
+            if (k < ntiles - kResident) {   // the last kResident tiles stay for pass B
+              tc::fence_before_sync();
+              __syncwarp();
+              if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
+            }
             const int t = k * kTileM + row;
   #pragma unroll
             for (int j = 0; j < 16; ++j) {
@@ -470,6 +483,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               }
             }
           }
+          if (ct == 0) FC_STAMP(it, 3);
           // combine (reference max, sum) over the warp, then over the 4 lane quarters
           float mw[16];
   #pragma unroll
@@ -507,11 +521,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mj[j] = s_m[grp * 16 + j];
             zj[j] = s_zinv[grp * 16 + j];
           }
-          // pass B: normalised probabilities of the re-streamed tiles -> window mean
-          for (int k = 0; k < ntiles; ++k) {
-            const int gk = gtile + ntiles + k, sl = gk % kSlots;
-            tc::mbar_wait(&sl_full[sl], (gk / kSlots) & 1);
-            tc::fence_after_sync();
+          if (ct == 0) FC_STAMP(it, 8);
+          // pass B: normalised probabilities -> window mean; first the resident tail
+          // tiles (their slots free as they go, so the re-stream can start), then the
+          // re-streamed tiles [0, ntiles - kResident)
+          for (int kk = 0; kk < ntiles; ++kk) {
+            const bool resident = kk < kResident;
+            const int k = resident ? ntiles - kResident + kk : kk - kResident;
+            const int gk = resident ? gtile + k : gtile + ntiles + k, sl = gk % kSlots;
+            if (!resident) {
+              tc::mbar_wait(&sl_full[sl], (gk / kSlots) & 1);
+              tc::fence_after_sync();
+            }
             float v[16];
             tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
             tc::fence_before_sync();
@@ -526,7 +547,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
           }
         }
-        gtile += ntiles > kSlots ? 2 * ntiles : ntiles;
+        gtile += snap_loads(ntiles);
         if (kGqa) {
           Consumers::sync();
           for (int t = ct; t < T_len; t += kThreads) {
