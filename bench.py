@@ -548,7 +548,9 @@ def run_prefill_bench(args, rank, world, local_rank):
     from paper_2503_08461_b200 import _native
 
     times, launches = [], 0
-    for step in range(args.warmup + args.steps):
+
+    def step_once(timed):
+        nonlocal launches
         hs = pool.allocate_batch(rids, specs, 0.0)
         torch.cuda.synchronize(device)
         l0 = _native.launch_count()
@@ -558,10 +560,16 @@ def run_prefill_bench(args, rank, world, local_rank):
             pool.write_prefill_kv(hs, layer, k[layer], v[layer])
         e1.record(stream)
         e1.synchronize()
-        if step >= args.warmup:
+        if timed:
             times.append(e0.elapsed_time(e1))
             launches += _native.launch_count() - l0
         pool.release_batch(hs, 1.0)
+
+    for _ in range(args.warmup):
+        step_once(False)
+    with ClockSampler(device.index) as clocks:
+        for _ in range(args.steps):
+            step_once(True)
     ms = statistics.mean(times)
     max_ms = _allreduce(sum(times), "max", device)
     peak, peak_kind = measured_peak()
@@ -578,6 +586,7 @@ def run_prefill_bench(args, rank, world, local_rank):
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "alg_bytes_per_step": moved},
         "gpu_launches": launches,
+        "clocks": clocks.summary(),
     }
 
 
