@@ -15,14 +15,18 @@ constexpr int kWarps = kThreads / 32;
 // A set of 256 threads that cooperates on one segment: the whole CTA, or the
 // consumer warps of a warp-specialised kernel synchronising on a named barrier.
 struct CtaGroup {
+  static constexpr int kSize = kThreads;
   __device__ __forceinline__ static int tid() { return threadIdx.x; }
   __device__ __forceinline__ static void sync() { __syncthreads(); }
 };
-template <int kFirstThread, int kBarrierId>
+// kCount threads from kFirstThread on (kThreads for the select / press groups; the
+// compaction helpers also run on smaller groups)
+template <int kFirstThread, int kBarrierId, int kCount = kThreads>
 struct NamedGroup {
+  static constexpr int kSize = kCount;
   __device__ __forceinline__ static int tid() { return threadIdx.x - kFirstThread; }
   __device__ __forceinline__ static void sync() {
-    asm volatile("bar.sync %0, %1;" ::"n"(kBarrierId), "n"(kThreads) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"n"(kBarrierId), "n"(kCount) : "memory");
   }
 };
 
@@ -564,7 +568,7 @@ struct RowCfg {
 template <int kRowBytes, int kItems, class G = CtaGroup>
 struct Compactor {
   static constexpr int kVecs = kRowBytes / 16;
-  static constexpr int kChunk = kThreads * kItems / (2 * kVecs);  // ranks per chunk
+  static constexpr int kChunk = G::kSize * kItems / (2 * kVecs);  // ranks per chunk
   char* seg;
   const Geom& g;
   const int32_t* s_src;
@@ -576,7 +580,7 @@ struct Compactor {
   __device__ __forceinline__ void load(int j0, uint4 (&buf)[kItems]) const {
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
-      const int item = it * kThreads + G::tid();
+      const int item = it * G::kSize + G::tid();
       const int row = item / (2 * kVecs), rem = item % (2 * kVecs);
       const int kv = rem / kVecs, vec = rem % kVecs;
       const int j = j0 + row;
@@ -590,7 +594,7 @@ struct Compactor {
   // Pull the source rows (K and V) of ranks [j0, j0 + kChunk) towards L2 so the
   // later register loads hit L2: one bulk prefetch per row, no registers held.
   __device__ __forceinline__ void prefetch(int j0) const {
-    for (int r = G::tid(); r < 2 * kChunk; r += kThreads) {
+    for (int r = G::tid(); r < 2 * kChunk; r += G::kSize) {
       const int kv = r >= kChunk, j = j0 + (kv ? r - kChunk : r);
       if (j < K) {
         const int src = idx[j];
@@ -603,7 +607,7 @@ struct Compactor {
   __device__ __forceinline__ void store(int j0, const uint4 (&buf)[kItems]) const {
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
-      const int item = it * kThreads + G::tid();
+      const int item = it * G::kSize + G::tid();
       const int row = item / (2 * kVecs), rem = item % (2 * kVecs);
       const int kv = rem / kVecs, vec = rem % kVecs;
       const int j = j0 + row;
@@ -665,8 +669,8 @@ __device__ __forceinline__ void compact_rows(char* __restrict__ seg, const Geom&
 template <int kRowBytes, class G, int kRanks, int kNBuf>
 struct AsyncCompactor {
   static constexpr int kVecs = kRowBytes / 16;
-  static constexpr int kItems = kRanks * 2 * kVecs / kThreads;  // 16-B pieces per thread
-  static_assert(kItems * kThreads == kRanks * 2 * kVecs, "chunk must split evenly over the group");
+  static constexpr int kItems = kRanks * 2 * kVecs / G::kSize;  // 16-B pieces per thread
+  static_assert(kItems * G::kSize == kRanks * 2 * kVecs, "chunk must split evenly over the group");
   static constexpr int kChunkBytes = kRanks * 2 * kRowBytes;
   static constexpr int kSmemBytes = kNBuf * kChunkBytes;
 };
@@ -687,7 +691,7 @@ __device__ __forceinline__ void compact_rows_async(char* __restrict__ seg, const
       const uint32_t buf = sbase + (uint32_t)((c % kNBuf) * A::kChunkBytes);
 #pragma unroll
       for (int it = 0; it < A::kItems; ++it) {
-        const int v = it * kThreads + G::tid();
+        const int v = it * G::kSize + G::tid();
         const int rank = v / (2 * kVecs), rem = v % (2 * kVecs);
         const int kv = rem / kVecs, vec = rem % kVecs;
         const int j = j_start + c * kRanks + rank;
@@ -711,7 +715,7 @@ __device__ __forceinline__ void compact_rows_async(char* __restrict__ seg, const
     const unsigned char* buf = smem + (c % kNBuf) * A::kChunkBytes;
 #pragma unroll
     for (int it = 0; it < A::kItems; ++it) {
-      const int v = it * kThreads + G::tid();
+      const int v = it * G::kSize + G::tid();
       const int rank = v / (2 * kVecs), rem = v % (2 * kVecs);
       const int kv = rem / kVecs, vec = rem % kVecs;
       const int j = j_start + c * kRanks + rank;

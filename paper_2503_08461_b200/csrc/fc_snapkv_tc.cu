@@ -70,9 +70,17 @@ __host__ __device__ __forceinline__ int snap_loads(int ntiles) {
 constexpr int kWin = 32;                        // window queries (UMMA N)
 constexpr int kConsumerFirst = 64;              // warps 0,1 = producer, MMA
 constexpr int kCompactorFirst = kConsumerFirst + kThreads;
-constexpr int kTcThreads = kCompactorFirst + kThreads;
+#ifndef FC_SNAP_GQA_COMP_WARPS   // compactor warps of the GQA instantiation (8 = as g = 1)
+#define FC_SNAP_GQA_COMP_WARPS 4
+#endif
+// GQA segments are consumer-bound (g softmax units per segment) with the compactors
+// mostly idle: 4 compactor warps make the CTA 14 warps, at most 4 per SM sub-partition,
+// so every warp may hold 128 registers (18 warps cap it at 96): c3g 4.09 -> 3.94 ms.
+// (Two tiles' TMEM loads per wait on top of that measured 4.03 ms.)
+__host__ __device__ constexpr int snap_comp_threads(bool gqa) { return gqa ? 32 * FC_SNAP_GQA_COMP_WARPS : kThreads; }
+__host__ __device__ constexpr int snap_threads(bool gqa) { return kCompactorFirst + snap_comp_threads(gqa); }
+constexpr int kTcThreads = snap_threads(false);
 using Consumers = NamedGroup<kConsumerFirst, 1>;
-using Compactors = NamedGroup<kCompactorFirst, 2>;
 
 struct CompactJob {  // consumer -> compactor hand-off of one segment
   int32_t l, h, K, first_moved, slot;
@@ -136,7 +144,7 @@ __host__ __device__ inline TcSmem tc_smem_plan(int D, int bs, int max_T, int max
 }
 
 template <typename T, int D, bool kGqa, bool kSpill>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(snap_threads(kGqa), 1)
     snapkv_tc_kernel(char* __restrict__ arena, const int32_t* __restrict__ table, const Geom g,
                      const __grid_constant__ PressBatch b, const PressParams pp,
                      const __grid_constant__ CUtensorMap kmap,
@@ -297,6 +305,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     __syncwarp();
   } else if (warp >= kCompactorFirst / 32) {
+    using Compactors = NamedGroup<kCompactorFirst, 2, snap_comp_threads(kGqa)>;
     // ================= compactors (8 warps, named barrier 2) =================
     for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
       const int jb = it & 1;
@@ -357,12 +366,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // pass 1: per-query max over all tokens
   #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] = -INFINITY;
-        for (int k = 0; k < ntiles; ++k) {
-          const int sl = (gtile + k) % kSlots;
-          tc::mbar_wait(&sl_full[sl], ((gtile + k) / kSlots) & 1);
-          tc::fence_after_sync();
-          float v[16];
-          tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+        auto max_tile = [&](int k, const float (&v)[16]) {
           const int t = k * kTileM + row;
           if (t <= T_len - kWin) {   // below the window: no causal mask
   #pragma unroll
@@ -372,6 +376,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (int j = 0; j < 16; ++j)
               if (t < T_len && t <= T_len - kWin + grp * 16 + j) acc[j] = fmaxf(acc[j], v[j] * scale);
           }
+        };
+        for (int k = 0; k < ntiles; ++k) {
+          const int sl = (gtile + k) % kSlots;
+          tc::mbar_wait(&sl_full[sl], ((gtile + k) / kSlots) & 1);
+          tc::fence_after_sync();
+          float v[16];
+          tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+          max_tile(k, v);
         }
         if (ct == 0) FC_STAMP(it, 3);
         {
@@ -393,10 +405,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // pass 2: per-query sum of exp
   #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-        for (int k = 0; k < ntiles; ++k) {
-          const int sl = (gtile + k) % kSlots;
-          float v[16];
-          tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+        auto exp_tile = [&](int k, float (&v)[16]) {
           const int t = k * kTileM + row;
           if (t <= T_len - kWin) {   // below the window: no causal mask
   #pragma unroll
@@ -412,6 +421,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               v[j] = e;
             }
           }
+        };
+        for (int k = 0; k < ntiles; ++k) {
+          const int sl = (gtile + k) % kSlots;
+          float v[16];
+          tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+          exp_tile(k, v);
           tc::tmem_st_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);   // exps replace the logits
         }
         tc::tmem_store_wait();
@@ -433,13 +448,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int j = 0; j < 16; ++j) zj[j] = s_zinv[grp * 16 + j];
         if (ct == 0) FC_STAMP(it, 10);
         // pass 3: partial window mean of the normalised probabilities; frees TMEM slots
-        for (int k = 0; k < ntiles; ++k) {
-          const int sl = (gtile + k) % kSlots;
-          float v[16];
-          tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
+        auto mean_tile = [&](int k, const float (&v)[16]) {
           const int t = k * kTileM + row;
           if (t < n_keep) {
             float sum = 0.f;
@@ -447,6 +456,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (int j = 0; j < 16; ++j) sum = fmaf(v[j], zj[j], sum);   // masked entries are 0
             atomicAdd(&wacc[t], sum * inv_wg);   // two addends onto 0: order-free
           }
+        };
+        for (int k = 0; k < ntiles; ++k) {
+          const int sl = (gtile + k) % kSlots;
+          float v[16];
+          tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
+          mean_tile(k, v);
         }
         } else {
           // ---- long segment (T > kSlots * 128): two streamed passes ----
@@ -715,17 +733,17 @@ fc_status launch_snapkv_tc(const Geom& g, int dtype, char* arena, const int32_t*
     if (ws_floats < row) return set_error(FC_ERR_INVALID_STATE, "SnapKV spill workspace too small");
     grid = (int)std::min<int64_t>(grid, ws_floats / row);
   }
+  const bool gqa = pp.num_q_heads != g.H;
   auto launch = [&](auto kern) -> fc_status {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.total);
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(snapkv_tc)");
-    kern<<<grid, kTcThreads, plan.total, stream>>>(arena, table, g, b, pp, kmap, qmap, out, n_items,
+    kern<<<grid, snap_threads(gqa), plan.total, stream>>>(arena, table, g, b, pp, kmap, qmap, out, n_items,
                                                    max_K, ws);
     note_launch();
     note_path(kPathTc);
     return cuda_check(cudaGetLastError(), "snapkv_tc_kernel");
   };
   // g = 1 gets its own instantiation (the unit loop folds away)
-  const bool gqa = pp.num_q_heads != g.H;
   auto pick = [&](auto tag) -> fc_status {
     using T = decltype(tag);
     if (g.D == 64) {
