@@ -78,9 +78,15 @@ constexpr int kBHalf = kBRows * 128;            // one 64-column slab of B (byte
 constexpr int kBBytes = 2 * kBHalf;             // one full B matrix (hi or lo)
 constexpr int kConsumerFirst = 64;
 constexpr int kCompactorFirst = kConsumerFirst + kThreads;
-constexpr int kEaThreads = kCompactorFirst + kThreads;
+#ifndef FC_EA_GQA_COMP_WARPS   // compactor warps of the GQA instantiation (8 = as g = 1)
+#define FC_EA_GQA_COMP_WARPS 4
+#endif
+// GQA: g units of K . Sigma_h per segment keep the consumers busy while the compactors
+// idle; 4 compactor warps make the CTA 14 warps, so every warp may hold 128 registers.
+__host__ __device__ constexpr int ea_comp_threads(bool gqa) { return gqa ? 32 * FC_EA_GQA_COMP_WARPS : kThreads; }
+__host__ __device__ constexpr int ea_threads(bool gqa) { return kCompactorFirst + ea_comp_threads(gqa); }
+constexpr int kEaThreads = ea_threads(false);
 using Consumers = NamedGroup<kConsumerFirst, 1>;
-using Compactors = NamedGroup<kCompactorFirst, 2>;
 
 struct Job {
   int32_t l, h, K, first_moved, slot;
@@ -163,7 +169,7 @@ using namespace ea;
 // T = __half or __nv_bfloat16: the K/V tiles' type; Sigma / mu are split into
 // hi + lo parts of the same type (fp16: ~22 significant bits, bf16: ~16).
 template <typename T, bool kGqa, bool kSpill>
-__global__ void __launch_bounds__(kEaThreads, 1)
+__global__ void __launch_bounds__(ea_threads(kGqa), 1)
     ea_tc_kernel(char* __restrict__ arena, const int32_t* __restrict__ table, const Geom g,
                  const __grid_constant__ PressBatch b, const PressParams pp,
                  const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap cmap,
@@ -335,6 +341,7 @@ __global__ void __launch_bounds__(kEaThreads, 1)
     }
     __syncwarp();
   } else if (warp >= kCompactorFirst / 32) {
+    using Compactors = NamedGroup<kCompactorFirst, 2, ea_comp_threads(kGqa)>;
     // ================= compactors =================
     for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
       const int jb = it & 1;
@@ -615,7 +622,7 @@ fc_status launch_ea_tc(const Geom& g, int dtype, char* arena, const int32_t* tab
   auto launch = [&](auto kern) -> fc_status {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P.total);
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(ea_tc)");
-    kern<<<grid, kEaThreads, P.total, stream>>>(arena, table, g, b, pp, kmap, cmap, in.mean_q, out,
+    kern<<<grid, ea_threads(gqa), P.total, stream>>>(arena, table, g, b, pp, kmap, cmap, in.mean_q, out,
                                                 n_items, max_K, ws);
     note_launch();
     note_path(kPathTc);
