@@ -83,7 +83,14 @@ constexpr int kCompactorFirst = kConsumerFirst + kThreads;
 #endif
 // GQA: g units of K . Sigma_h per segment keep the consumers busy while the compactors
 // idle; 4 compactor warps make the CTA 14 warps, so every warp may hold 128 registers.
-__host__ __device__ constexpr int ea_comp_threads(bool gqa) { return gqa ? 32 * FC_EA_GQA_COMP_WARPS : kThreads; }
+#ifndef FC_EA_COMP_WARPS   // compactor warps of the g = 1 instantiation
+// (its compaction is bytes-in-flight bound: c4w 43.1 ms at 8 warps x 8 loads, 50.8 ms at
+// 6 x 8, 43.1 ms at 6 x 12 with the consumers at 128 registers, 74 ms at 4 x 12)
+#define FC_EA_COMP_WARPS 8
+#endif
+__host__ __device__ constexpr int ea_comp_threads(bool gqa) {
+  return 32 * (gqa ? FC_EA_GQA_COMP_WARPS : FC_EA_COMP_WARPS);
+}
 __host__ __device__ constexpr int ea_threads(bool gqa) { return kCompactorFirst + ea_comp_threads(gqa); }
 constexpr int kEaThreads = ea_threads(false);
 using Consumers = NamedGroup<kConsumerFirst, 1>;
