@@ -447,24 +447,31 @@ __global__ void __launch_bounds__(snap_threads(kGqa), 1)
   #pragma unroll
         for (int j = 0; j < 16; ++j) zj[j] = s_zinv[grp * 16 + j];
         if (ct == 0) FC_STAMP(it, 10);
-        // pass 3: partial window mean of the normalised probabilities; frees TMEM slots
-        auto mean_tile = [&](int k, const float (&v)[16]) {
-          const int t = k * kTileM + row;
-          if (t < n_keep) {
+        // pass 3: window mean of the normalised probabilities; frees TMEM slots. The two
+        // warp groups split the tiles (group g: k = g, g + 2, ...) and a thread sums all 32
+        // queries of its row, so each token's mean is one plain store: shared-memory fp32
+        // atomics are CAS loops on sm_100 (ATOMS.CAST.SPIN), with two warps contending.
+        {
+          float zall[kWin];
+  #pragma unroll
+          for (int j = 0; j < kWin; ++j) zall[j] = s_zinv[j];
+          const uint32_t row_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+          for (int k = grp; k < ntiles; k += 2) {
+            const int sl = (gtile + k) % kSlots;
+            float v[16];
             float sum = 0.f;
   #pragma unroll
-            for (int j = 0; j < 16; ++j) sum = fmaf(v[j], zj[j], sum);   // masked entries are 0
-            atomicAdd(&wacc[t], sum * inv_wg);   // two addends onto 0: order-free
+            for (int hq = 0; hq < 2; ++hq) {
+              tc::tmem_ld_32x32b_x16(row_addr + (uint32_t)(sl * kWin + hq * 16), v);
+  #pragma unroll
+              for (int j = 0; j < 16; ++j) sum = fmaf(v[j], zall[hq * 16 + j], sum);   // masked entries are 0
+            }
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sl_empty[sl], 2);   // stands for both groups' warps
+            const int t = k * kTileM + row;
+            if (t < n_keep) wacc[t] = sum * inv_wg;
           }
-        };
-        for (int k = 0; k < ntiles; ++k) {
-          const int sl = (gtile + k) % kSlots;
-          float v[16];
-          tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
-          mean_tile(k, v);
         }
         } else {
           // ---- long segment (T > kSlots * 128): two streamed passes ----

@@ -271,6 +271,9 @@ __device__ __forceinline__ void tmem_store_wait() {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
 
 // UMMA shared-memory descriptor: K-major operand in the 128-byte-swizzle
 // canonical layout (8-row x 128-byte atoms, 1 KiB apart). `addr` may sit
