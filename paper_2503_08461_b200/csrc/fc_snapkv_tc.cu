@@ -549,8 +549,11 @@ __global__ void __launch_bounds__(snap_threads(kGqa), 1)
           if (ct == 0) FC_STAMP(it, 8);
           // pass B: normalised probabilities -> window mean; first the resident tail
           // tiles (their slots free as they go, so the re-stream can start), then the
-          // re-streamed tiles [0, ntiles - kResident)
-          for (int kk = 0; kk < ntiles; ++kk) {
+          // re-streamed tiles [0, ntiles - kResident). As in pass 3 of the resident path,
+          // the two warp groups split the tiles and a thread covers all 32 queries of its
+          // row (statistics of the other group's queries from SMEM), so the window mean is
+          // a plain store instead of two contending shared-memory float atomics.
+          for (int kk = grp; kk < ntiles; kk += 2) {
             const bool resident = kk < kResident;
             const int k = resident ? ntiles - kResident + kk : kk - kResident;
             const int gk = resident ? gtile + k : gtile + ntiles + k, sl = gk % kSlots;
@@ -558,18 +561,26 @@ __global__ void __launch_bounds__(snap_threads(kGqa), 1)
               tc::mbar_wait(&sl_full[sl], (gk / kSlots) & 1);
               tc::fence_after_sync();
             }
-            float v[16];
-            tc::tmem_ld_32x32b_x16(lane_addr + (uint32_t)(sl * kWin), v);
+            const uint32_t row_addr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sl * kWin);
+            float sum = 0.f;
+  #pragma unroll
+            for (int hq = 0; hq < 2; ++hq) {
+              float v[16];
+              tc::tmem_ld_32x32b_x16(row_addr + (uint32_t)(hq * 16), v);
+              if (hq == grp) {
+  #pragma unroll
+                for (int j = 0; j < 16; ++j) sum = fmaf(tc::ex2(fmaf(v[j], scale, -mj[j])), zj[j], sum);
+              } else {
+  #pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  sum = fmaf(tc::ex2(fmaf(v[j], scale, -s_m[hq * 16 + j])), s_zinv[hq * 16 + j], sum);
+              }
+            }
             tc::fence_before_sync();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&sl_empty[sl]);
+            if (lane == 0) tc::mbar_arrive(&sl_empty[sl], 2);   // stands for both groups' warps
             const int t = k * kTileM + row;
-            if (t < n_keep) {
-              float sum = 0.f;
-  #pragma unroll
-              for (int j = 0; j < 16; ++j) sum = fmaf(tc::ex2(fmaf(v[j], scale, -mj[j])), zj[j], sum);
-              atomicAdd(&wacc[t], sum * inv_wg);   // two addends onto 0: order-free
-            }
+            if (t < n_keep) wacc[t] = sum * inv_wg;
           }
         }
         gtile += snap_loads(ntiles);
