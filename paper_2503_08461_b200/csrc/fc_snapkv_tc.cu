@@ -362,6 +362,7 @@ __global__ void __launch_bounds__(snap_threads(kGqa), 1)
       const int gq = kGqa ? pp.num_q_heads / g.H : 1;
       const float inv_wg = 1.0f / (float)(kWin * gq);
       for (int gi = 0; gi < gq; ++gi) {
+        if (ct == 0 && gi == 1) FC_STAMP(it, 11);
         if (ntiles <= kSlots) {
         // pass 1: per-query max over all tokens
   #pragma unroll
@@ -386,6 +387,7 @@ __global__ void __launch_bounds__(snap_threads(kGqa), 1)
           max_tile(k, v);
         }
         if (ct == 0) FC_STAMP(it, 3);
+        if (ct == 0 && gi == 1) FC_STAMP(it, 15);
         {
           const float r = tc::warp_reduce16(acc, lane, [](float a, float b) { return fmaxf(a, b); });
           if ((lane & 1) == 0) s_red[cw][lane >> 1] = r;

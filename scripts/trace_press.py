@@ -60,3 +60,9 @@ if len(sys.argv) > 2 and sys.argv[2] == "sub":
     print("select: keys->job_empty %.2f  ctab copy %.2f  select+emit+handoff %.2f us" % (
         (d[:, :, 13] - d[:, :, 12]).mean(), (d[:, :, 14] - d[:, :, 13]).mean(),
         (d[:, :, 5] - d[:, :, 14]).mean()))
+if len(sys.argv) > 2 and sys.argv[2] == "units":
+    prev5 = d[:, :-1, 5]
+    nxt = d[:, 1:]
+    print("GQA units: unit0 %.2f  unit1 pass 1 %.2f  unit1 start -> all units done %.2f  after units -> handoff %.2f us" % (
+        (nxt[:, :, 11] - prev5).mean(), (nxt[:, :, 15] - nxt[:, :, 11]).mean(),
+        (nxt[:, :, 4] - nxt[:, :, 11]).mean(), (nxt[:, :, 5] - nxt[:, :, 4]).mean()))
