@@ -156,7 +156,7 @@ def measured_peak():
 class ClockSampler:
     """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
 
-    def __init__(self, index: int, period: float = 0.05):
+    def __init__(self, index: int, period: float = 0.01):
         self.index, self.period = index, period
         self.samples, self.reasons = [], set()
         self.max_mhz = None
@@ -187,19 +187,22 @@ class ClockSampler:
             "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
             "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
         }
-        while not self._stop.is_set():
+        # every 10 ms while the timed region runs, plus once more as it ends, so even a
+        # ~20-ms region (c3g's 5 steps) carries a few samples
+        while True:
+            stopping = self._stop.is_set()
             try:
-                util = nv.nvmlDeviceGetUtilizationRates(self._h).gpu
                 mhz = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
                 mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-                if util > 0:
-                    self.samples.append(mhz)
-                    for k, bit in names.items():
-                        if mask & bit:
-                            self.reasons.add(k)
+                self.samples.append(mhz)
+                for k, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(k)
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(self.period)
+            if stopping:
+                break
+            self._stop.wait(self.period)
 
     def __exit__(self, *exc):
         self._stop.set()
