@@ -638,7 +638,7 @@ def press_leg(args, name, rank, world, local_rank, with_e2e):
     hq = Q_HEADS.get(name, cfg.num_kv_heads)
     pool = KVCachePool(cfg, cap, device=device, kv_dtype=dtype, max_handles=max(64, 2 * n),
                        max_tokens_per_handle=max(s.total_tokens for s in specs) + 64,
-                       num_q_heads=hq)
+                       num_q_heads=hq, block_size=args.block_size)
     pool.set_profiling(True)
     ins = press_inputs(comp, cfg, n, device, torch, seed=1234 + rank, hq=hq)
     rids = [rank * 1_000_000 + i for i in range(n)]
@@ -702,7 +702,8 @@ def press_leg(args, name, rank, world, local_rank, with_e2e):
         "data": "synthetic (deterministic counter-based KV generator, oracle/synth.py)",
         "config": {
             "workload": f"{name}: {CONFIGS[name]}",
-            "press": comp.press.value, "factor": comp.factor, "requests_per_gpu": n,
+            "press": comp.press.value, "factor": comp.factor, "block_size": args.block_size,
+            "requests_per_gpu": n,
             "raw_tokens_per_gpu": raw_tokens,
             "parallelism": f"request-sharded x{world} ({'LPT shards of one batch' if strong else 'one batch per GPU'}; no data-path collective)",
             "l2": "inputs larger than L2 (raw KV %.1f GB/GPU) and re-filled between steps"
@@ -1023,6 +1024,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--block-size", type=int, default=16,
+                    help="pool block size in tokens for the press configs (default 16)")
     ap.add_argument("--legs", default=None,
                     help="extra press configs measured in the same run (default for c2: c3,c4w)")
     ap.add_argument("--parity-segments", type=int, default=64,

@@ -66,3 +66,11 @@ if len(sys.argv) > 2 and sys.argv[2] == "units":
     print("GQA units: unit0 %.2f  unit1 pass 1 %.2f  unit1 start -> all units done %.2f  after units -> handoff %.2f us" % (
         (nxt[:, :, 11] - prev5).mean(), (nxt[:, :, 15] - nxt[:, :, 11]).mean(),
         (nxt[:, :, 4] - nxt[:, :, 11]).mean(), (nxt[:, :, 5] - nxt[:, :, 4]).mean()))
+if len(sys.argv) > 2 and sys.argv[2] == "gqa":   # libfastcache_trace_gqa.so (-DFC_TRACE_GQA)
+    nxt = d[:, 1:]
+    u1 = nxt[:, :, 11]
+    print("unit 1 relative to its consumer start (us): producer first K tile %.2f last %.2f | "
+          "MMA first tile %.2f last %.2f | consumer end of pass 1 %.2f" % (
+              (nxt[:, :, 0] - u1).mean(), (nxt[:, :, 1] - u1).mean(), (nxt[:, :, 6] - u1).mean(),
+              (nxt[:, :, 7] - u1).mean(), (nxt[:, :, 15] - u1).mean()))
+
