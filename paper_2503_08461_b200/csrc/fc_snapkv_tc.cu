@@ -243,8 +243,13 @@ __global__ void __launch_bounds__(snap_threads(kGqa), 1)
           const int n_chunks = min(chunks, nb - k * chunks);
           if (lane == 0) {
             tc::mbar_wait(&st_empty[st], ((gtile / kTcStages) & 1) ^ 1);
+#ifdef FC_TRACE_GQA   // GQA diagnosis (scripts/trace_press.py gqa): unit 1's first / last K tile issue
+            if (gi == 1 && kl == 0) FC_STAMP(it, 0);
+            if (gi == 1 && kl == ntiles - 1) FC_STAMP(it, 1);
+#else
             if (gi == 0 && kl == 0) FC_STAMP(it, 0);
             if (gi == 0 && kl == ntiles - 1) FC_STAMP(it, 1);
+#endif
             tc::mbar_expect_tx(&st_full[st], (uint32_t)(n_chunks * g.bs * D * 2));
           }
           __syncwarp();
@@ -297,6 +302,10 @@ __global__ void __launch_bounds__(snap_threads(kGqa), 1)
           }
           tc::mma_commit(&st_empty[st]);
           tc::mma_commit(&sl_full[sl]);
+#ifdef FC_TRACE_GQA
+          if (gi == 1 && k == 0) FC_STAMP(it, 6);   // (the compactor's slots in this build)
+          if (gi == 1 && k == nload - 1) FC_STAMP(it, 7);
+#endif
         }
         tc::mma_commit(&q_empty[qb]);
         }
@@ -310,7 +319,9 @@ __global__ void __launch_bounds__(snap_threads(kGqa), 1)
     for (int it = 0, item = blockIdx.x; item < n_items; ++it, item += gridDim.x) {
       const int jb = it & 1;
       tc::mbar_wait(&job_full[jb], (it >> 1) & 1);
+#ifndef FC_TRACE_GQA
       if (Compactors::tid() == 0) FC_STAMP(it, 6);
+#endif
       const CompactJob job = s_job[jb];
       char* seg = arena + g.seg_base(job.l, 0, job.h);
       const int32_t* tab = kSpill ? table + (int64_t)job.slot * g.max_bpr : ctab + jb * nb_stride;
@@ -325,7 +336,9 @@ __global__ void __launch_bounds__(snap_threads(kGqa), 1)
 #endif
       Compactors::sync();
       if (Compactors::tid() == 0) {
+#ifndef FC_TRACE_GQA
         FC_STAMP(it, 7);
+#endif
         tc::mbar_arrive(&job_empty[jb]);
       }
     }
