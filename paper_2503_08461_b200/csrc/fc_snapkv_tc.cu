@@ -93,10 +93,10 @@ struct CompactJob {  // consumer -> compactor hand-off of one segment
 #define FC_SNAP_L2HINT 1
 #endif
 #ifndef FC_SNAP_CRANKS
-#define FC_SNAP_CRANKS 32
+#define FC_SNAP_CRANKS 16   // measured at c3: 16 x 6 buffers 5.87 ms, 32 x 4 5.97, 16 x 8 5.95, 16 x 4 6.02, 32 x 3 6.00
 #endif
 #ifndef FC_SNAP_CBUFS
-#define FC_SNAP_CBUFS 4
+#define FC_SNAP_CBUFS 6
 #endif
 
 struct TcSmem {
