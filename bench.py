@@ -585,9 +585,13 @@ def run_prefill_bench(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "f16", "data": "synthetic (random K/V)",
         "config": {"workload": f"c2p: {CONFIGS['c2p']}", "requests_per_gpu": n,
                    "timing": "CUDA events around the 32 per-layer write_prefill_kv calls"},
-        "roofline": {"bound": "hbm", "kernel": "write_prefill_kernel", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": "write_prefill_tma_kernel (TMA head-group tiles -> "
+                                                 "whole-chunk bulk stores)", "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "alg_bytes_per_step": moved},
+                     "traffic": _scaled_traffic("r02_c2p", moved),
+                     "traffic_note": "DRAM bytes per step = the ncu traffic/algorithmic ratio of one "
+                                     "layer's launch (profiles/ncu_r02_c2p.json) x the step's bytes",
+                     "alg_bytes_per_step": moved},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }

@@ -1,9 +1,13 @@
 // fc_io.cu -- payload movement kernels: the K8 synthetic KV generator, dense
 // <-> paged token copies (prefill ingest, P.Store of PAPER.md:246), and the
 // standalone K7 compress_tensor (reference kv.py:211-239).
+#include <cudaTypedefs.h>
+
 #include <cstring>
+#include <mutex>
 
 #include "fc_internal.cuh"
+#include "fc_tc.cuh"
 
 namespace fc {
 
@@ -359,9 +363,225 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---------------------------------------------------------------------------
+// P.Store through the copy engines: one TMA load brings a (request, pool block,
+// K|V, head group) tile -- bs tokens x hg heads of the varlen [rows][H][D] source,
+// landed head-major by a 3-D tensor map whose head stride is the inner one -- into a
+// 3-stage SMEM ring; each head's bs rows then leave as ONE contiguous bulk store of
+// its bs * D * bpe pool chunk (partial blocks at a request's edges go row by row).
+// One thread per CTA issues everything: per 64-KB tile one load and hg stores, so
+// HBM sees whole 4-KB chunk writes and 8-KB row reads instead of 16-B thread traffic.
+// ---------------------------------------------------------------------------
+// measured at c2p (16-KB tiles, 5 loads ahead, 2 CTAs per SM): 5.57 ms = 1.00 of the
+// copy peak; 3 stages 6.05 ms, 4: 6.16, 7: 5.58; 8 / 12 stages (one CTA per SM) 8.2-9.2 ms;
+// 8-KB tiles 6.4-7.9 ms, 32-KB 5.9-6.1 ms; the register kernel below 6.48 ms (0.86)
+#ifndef FC_PF_STAGES
+#define FC_PF_STAGES 6
+#endif
+constexpr int kPfStages = FC_PF_STAGES;
+#ifndef FC_PF_DEFER   // park the block id one tile later (measured slower: 5.83 vs 5.58 ms)
+#define FC_PF_DEFER 0
+#endif
+#ifndef FC_PF_AHEAD
+#define FC_PF_AHEAD (FC_PF_STAGES - 1)
+#endif
+constexpr int kPfAhead = FC_PF_AHEAD;
+static_assert(kPfAhead >= 1 && kPfAhead < kPfStages, "prefill ring: loads ahead < stages");
+struct PrefillTmaBatch {
+  int32_t n, layer, hg, nhg;
+  int32_t item0[kMaxBatch + 1];   // first work item of request i (prefix over requests)
+  PrefillReq req[kMaxBatch];
+};
+
+__global__ void __launch_bounds__(32, 1)
+    write_prefill_tma_kernel(char* __restrict__ arena, const int32_t* __restrict__ table, const Geom g,
+                             const __grid_constant__ PrefillTmaBatch b,
+                             const __grid_constant__ CUtensorMap kmap,
+                             const __grid_constant__ CUtensorMap vmap, int stage_bytes) {
+  extern __shared__ __align__(128) unsigned char pf_smem[];
+  __shared__ __align__(8) uint64_t full[kPfStages];
+  __shared__ int64_t s_dst[kPfStages];   // pool chunk base of the tile's first head
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < kPfStages; ++i) tc::mbar_init(&full[i], 1);
+  tc::fence_barrier_init();
+  tc::tma_prefetch_desc(&kmap);
+  tc::tma_prefetch_desc(&vmap);
+  const int n_items = b.item0[b.n];
+  const int cnt = n_items > (int)blockIdx.x ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  struct Tile { int r, kv, hg0; int64_t blk, lo, hi; };
+  auto decode = [&](int i) {
+    const int item = (int)blockIdx.x + i * (int)gridDim.x;
+    int lo_r = 0, hi_r = b.n - 1;   // last request with item0 <= item
+    while (lo_r < hi_r) {
+      const int mid = (lo_r + hi_r + 1) >> 1;
+      if (b.item0[mid] <= item) lo_r = mid; else hi_r = mid - 1;
+    }
+    const PrefillReq& q = b.req[lo_r];
+    int x = item - b.item0[lo_r];
+    Tile t;
+    t.r = lo_r;
+    t.hg0 = (x % b.nhg) * b.hg;
+    x /= b.nhg;
+    t.kv = x & 1;
+    t.blk = (q.tok0 >> g.bs_shift) + (x >> 1);
+    t.lo = max(q.tok0, t.blk << g.bs_shift);
+    t.hi = min(q.tok0 + q.n, (t.blk + 1) << g.bs_shift);
+    return t;
+  };
+  // the block id of a tile is read when its load is issued (FC_PF_DEFER: parked in
+  // s_dst one tile later)
+  int32_t pend_blk = 0;
+  int pend_st = -1;
+  int64_t pend_base = 0;
+  auto park = [&]() {
+    if (pend_st >= 0) s_dst[pend_st] = pend_base + (int64_t)pend_blk * g.block_stride;
+    pend_st = -1;
+  };
+  auto issue_load = [&](int i) {
+    park();
+    const int st = i % kPfStages;
+    const Tile t = decode(i);
+    const PrefillReq& q = b.req[t.r];
+    tc::mbar_expect_tx(&full[st], (uint32_t)stage_bytes);
+    tc::tma_load_3d(pf_smem + (int64_t)st * stage_bytes, t.kv ? &vmap : &kmap, &full[st], 0,
+                    (int)(q.row0 + (t.lo - q.tok0)), t.hg0);
+    pend_blk = __ldg(table + (int64_t)q.slot * g.max_bpr + t.blk);
+    pend_base = g.seg_base(b.layer, t.kv, t.hg0);
+    pend_st = st;
+    if (!FC_PF_DEFER) park();
+  };
+  // kPfAhead loads in flight ahead of the tile being stored; the other
+  // kPfStages - kPfAhead stages hold tiles whose bulk stores are still reading SMEM
+  for (int i = 0; i < kPfAhead && i < cnt; ++i) issue_load(i);
+  const int64_t chunk = (int64_t)g.bs * g.row_bytes;
+  for (int i = 0; i < cnt; ++i) {
+    const int st = i % kPfStages;
+    const Tile t = decode(i);
+    tc::mbar_wait(&full[st], (uint32_t)((i / kPfStages) & 1));
+    park();
+    const unsigned char* src = pf_smem + (int64_t)st * stage_bytes;
+    char* dst = arena + s_dst[st];
+    const int64_t rows = t.hi - t.lo, r0 = t.lo & (g.bs - 1);
+    for (int hh = 0; hh < b.hg; ++hh) {
+      // head hh's chunk is H-adjacent in the pool: (K|V, head) chunks follow each other
+      char* d = dst + (int64_t)hh * chunk;
+      const unsigned char* s_h = src + (int64_t)hh * chunk;
+      if (rows == g.bs) {
+        tc::bulk_s2g(d, s_h, (uint32_t)chunk);
+      } else {
+        for (int64_t rr = 0; rr < rows; ++rr)
+          tc::bulk_s2g(d + (r0 + rr) * g.row_bytes, s_h + rr * g.row_bytes, (uint32_t)g.row_bytes);
+      }
+    }
+    tc::bulk_commit();
+    const int nxt = i + kPfAhead;
+    if (nxt < cnt) {
+      // tile nxt - kPfStages (the stage's last user) has kPfStages - kPfAhead newer
+      // store groups; it must have finished reading SMEM
+      tc::bulk_wait_read<kPfStages - kPfAhead>();
+      issue_load(nxt);
+    }
+  }
+  tc::bulk_wait_all();
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 io_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// [rows][H][D] varlen source viewed as {D, rows, H} (head stride innermost after D), box
+// {D, bs, hg}: the tile lands head-major, each head's bs rows contiguous.
+static bool encode_prefill_src(CUtensorMap* map, const void* base, const Geom& g, int64_t rows, int hg) {
+  auto enc = io_encode();
+  if (!enc) return false;
+  const CUtensorMapDataType dt = g.bpe == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : g.bpe == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                              : CU_TENSOR_MAP_DATA_TYPE_UINT32;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.D, (cuuint64_t)rows, (cuuint64_t)g.H};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.H * g.row_bytes, (cuuint64_t)g.row_bytes};
+  const cuuint32_t box[3] = {(cuuint32_t)g.D, (cuuint32_t)g.bs, (cuuint32_t)hg};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+#ifndef FC_PF_TMA
+#define FC_PF_TMA 1
+#endif
+#ifndef FC_PF_STAGE_BYTES
+#define FC_PF_STAGE_BYTES 16384
+#endif
+
+// Returns false (nothing launched) when the geometry does not suit the TMA path.
+static bool launch_write_prefill_tma(const Geom& g, char* arena, const int32_t* table, int layer, int n,
+                                     const PrefillReq* reqs, const void* k, const void* v,
+                                     cudaStream_t stream, fc_status* status) {
+  if (!FC_PF_TMA || g.D > 256 || g.bs > 256) return false;
+  if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15) return false;
+  const int64_t chunk = (int64_t)g.bs * g.row_bytes;
+  int hg = 1;
+  while (hg * 2 <= g.H && g.H % (hg * 2) == 0 && hg * 2 <= 256 && chunk * hg * 2 <= FC_PF_STAGE_BYTES) hg *= 2;
+  if (chunk * hg > FC_PF_STAGE_BYTES) return false;
+  const int stage_bytes = (int)(chunk * hg);
+  const int smem = kPfStages * stage_bytes;
+  *status = FC_OK;
+  for (int c = 0; c < n; c += kMaxBatch) {
+    PrefillTmaBatch b;
+    memset(&b, 0, sizeof(b));
+    b.n = n - c < kMaxBatch ? n - c : kMaxBatch;
+    b.layer = layer;
+    b.hg = hg;
+    b.nhg = g.H / hg;
+    int64_t rows = 1, items = 0;
+    for (int i = 0; i < b.n; ++i) {
+      const PrefillReq& q = reqs[c + i];
+      b.req[i] = q;
+      b.item0[i] = (int32_t)items;
+      if (q.n > 0) {
+        const int64_t nblk = ((q.tok0 + q.n - 1) >> g.bs_shift) - (q.tok0 >> g.bs_shift) + 1;
+        items += nblk * 2 * b.nhg;
+      }
+      rows = std::max<int64_t>(rows, q.row0 + q.n);
+    }
+    if (items > INT32_MAX) return false;
+    b.item0[b.n] = (int32_t)items;
+    if (items == 0) continue;
+    CUtensorMap kmap, vmap;
+    if (!encode_prefill_src(&kmap, k, g, rows, hg) || !encode_prefill_src(&vmap, v, g, rows, hg)) {
+      if (c == 0) return false;
+      *status = set_error(FC_ERR_CUDA, "cuTensorMapEncodeTiled(prefill) failed");
+      return true;
+    }
+    cudaError_t e = cudaFuncSetAttribute(write_prefill_tma_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) {
+      *status = cuda_check(e, "cudaFuncSetAttribute(write_prefill_tma)");
+      return true;
+    }
+    const int grid = (int)std::min<int64_t>(items, (int64_t)sm_count() * std::max(1, (227 * 1024) / (smem + 1024)));
+    write_prefill_tma_kernel<<<grid, 32, smem, stream>>>(arena, table, g, b, kmap, vmap, stage_bytes);
+    note_launch();
+    *status = cuda_check(cudaGetLastError(), "write_prefill_tma_kernel");
+    if (*status != FC_OK) return true;
+  }
+  return true;
+}
+
 fc_status launch_write_prefill(const Geom& g, char* arena, const int32_t* table, int layer, int n,
                                const PrefillReq* reqs, const void* k, const void* v,
                                cudaStream_t stream) {
+  fc_status tma_status;
+  if (launch_write_prefill_tma(g, arena, table, layer, n, reqs, k, v, stream, &tma_status)) return tma_status;
   for (int c = 0; c < n; c += kMaxBatch) {
     PrefillBatch b;
     memset(&b, 0, sizeof(b));

@@ -88,3 +88,46 @@ def test_chunked_prefill_and_errors(cuda):
         pool.write_prefill_kv(hs, 1, full_k, full_v)
     with pytest.raises(ValueError):   # wrong row count for the default lengths
         pool.write_prefill_kv(hs, 0, full_k[:169].contiguous(), full_v[:169].contiguous())
+
+
+@pytest.mark.parametrize("H,D,bs,dtype", [(8, 128, 16, "float16"), (6, 64, 32, "bfloat16"),
+                                          (1, 256, 8, "float32"), (32, 128, 128, "float16")])
+def test_prefill_geometries_and_ragged_chunks(cuda, H, D, bs, dtype):
+    """The TMA ingest (head-group tiles, whole-chunk bulk stores, row stores at a chunk's
+    ragged edges) over head counts that are not powers of two, block sizes 8..128, more
+    requests than one launch descriptor holds (130 > 128), empty chunks, and three
+    chunked writes per request at unaligned token offsets."""
+    bpe = 4 if dtype == "float32" else 2
+    cfg = ModelConfig("m", 2, H, D, bpe)
+    n_req = 130
+    rng = np.random.default_rng(H * 1000 + bs)
+    lens = [int(x) for x in rng.integers(1, 3 * bs + 5, n_req)]
+    pool = KVCachePool(cfg, (sum(lens) + n_req * bs + 64) * cfg.bytes_per_token, device=cuda,
+                       kv_dtype=dtype, block_size=bs, max_handles=n_req,
+                       max_tokens_per_handle=4 * bs)
+    hs = pool.allocate_batch(list(range(n_req)), [split_modalities(0, n) for n in lens], 0.0)
+    tdt = getattr(torch, dtype)
+    g = torch.Generator(device=cuda).manual_seed(7)
+    full = [[(torch.randn((n, H, D), generator=g, device=cuda).to(tdt),
+              torch.randn((n, H, D), generator=g, device=cuda).to(tdt)) for n in lens]
+            for _ in range(cfg.num_layers)]
+    # three chunks per request with random cut points
+    cuts = [sorted(int(c) for c in rng.integers(0, n + 1, 2)) for n in lens]
+    bounds = [[0, a, b, n] for (a, b), n in zip(cuts, lens)]
+    for layer in range(cfg.num_layers):
+        for part in range(3):
+            ks, vs, seq, beg = [], [], [], []
+            for i in range(n_req):
+                lo, hi = bounds[i][part], bounds[i][part + 1]
+                ks.append(full[layer][i][0][lo:hi])
+                vs.append(full[layer][i][1][lo:hi])
+                seq.append(hi - lo)
+                beg.append(lo)
+            pool.write_prefill_kv(hs, layer, torch.cat(ks).contiguous(), torch.cat(vs).contiguous(),
+                                  seq_lens=seq, tok_begin=beg)
+    for i in range(n_req):
+        got = pool.load_tokens(hs[i])                            # [L, 2, H, n, D]
+        for layer in range(cfg.num_layers):
+            assert torch.equal(got[layer, 0], full[layer][i][0].permute(1, 0, 2)), (i, layer)
+            assert torch.equal(got[layer, 1], full[layer][i][1].permute(1, 0, 2)), (i, layer)
+    pool.verify_conservation()
