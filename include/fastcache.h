@@ -250,6 +250,11 @@ FC_API fc_status fc_pool_last_profile(fc_pool* pool, fc_profile* out);
  * out[2] chunk-fold (MEAN_POOL / SEEDED_LINEAR) kernels. Not synchronising. */
 FC_API fc_status fc_pool_last_paths(fc_pool* pool, int64_t out[3]);
 
+/* Kernel of the most recent fc_pool_write_prefill call: *tma = 1 the TMA ingest
+ * (head-group tiles, whole-chunk bulk stores), 0 the register-copy kernel (chunks above
+ * the 16-KB tile), -1 no prefill written yet. Not synchronising. */
+FC_API fc_status fc_pool_last_prefill_path(fc_pool* pool, int32_t* tma);
+
 /* Device pointer of a handle's block-table row and its live block count. */
 FC_API fc_status fc_pool_block_table(fc_pool* pool, int64_t handle_id, const int32_t** dev_row,
                               int32_t* n_blocks, int64_t* n_tokens);

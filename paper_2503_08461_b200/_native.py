@@ -45,6 +45,7 @@ EXPORTS = (
     "fc_pool_set_profiling", "fc_pool_last_profile", "fc_pool_compress_host_batch",
     "fc_pool_write_kv", "fc_pool_decode_attention", "fc_pool_write_prefill_kv",
     "fc_pool_last_paths",
+    "fc_pool_last_prefill_path",
 )
 
 
@@ -136,6 +137,7 @@ _SIGS = {
     "fc_pool_set_profiling": (_I32, [_P, _I32]),
     "fc_pool_last_profile": (_I32, [_P, ctypes.POINTER(ProfileC)]),
     "fc_pool_last_paths": (_I32, [_P, _PI64]),
+    "fc_pool_last_prefill_path": (_I32, [_P, ctypes.POINTER(ctypes.c_int32)]),
 }
 
 _lib = None

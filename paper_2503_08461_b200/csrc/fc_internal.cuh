@@ -246,9 +246,10 @@ fc_status launch_synth(const Geom& g, int dtype, char* arena, const int32_t* tab
 fc_status launch_store(const Geom& g, char* arena, const int32_t* table_row, int64_t tok_begin,
                        int64_t n_tok, const void* src, bool to_blocks, cudaStream_t stream,
                        int kv0 = 0, int nkv = 2);
+// *used_tma (optional): 1 when the TMA ingest ran, 0 for the register-copy kernel
 fc_status launch_write_prefill(const Geom& g, char* arena, const int32_t* table, int layer, int n,
                                const PrefillReq* reqs, const void* k, const void* v,
-                               cudaStream_t stream);
+                               cudaStream_t stream, int* used_tma = nullptr);
 fc_status launch_gather_host(const Geom& g, char* arena, const int32_t* table, int n,
                              const HostGatherReq* reqs, const int32_t* kept_idx, int kv,
                              cudaStream_t stream);

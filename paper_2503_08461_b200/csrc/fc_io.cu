@@ -579,9 +579,11 @@ static bool launch_write_prefill_tma(const Geom& g, char* arena, const int32_t* 
 
 fc_status launch_write_prefill(const Geom& g, char* arena, const int32_t* table, int layer, int n,
                                const PrefillReq* reqs, const void* k, const void* v,
-                               cudaStream_t stream) {
+                               cudaStream_t stream, int* used_tma) {
   fc_status tma_status;
-  if (launch_write_prefill_tma(g, arena, table, layer, n, reqs, k, v, stream, &tma_status)) return tma_status;
+  const bool tma = launch_write_prefill_tma(g, arena, table, layer, n, reqs, k, v, stream, &tma_status);
+  if (used_tma) *used_tma = tma ? 1 : 0;
+  if (tma) return tma_status;
   for (int c = 0; c < n; c += kMaxBatch) {
     PrefillBatch b;
     memset(&b, 0, sizeof(b));

@@ -155,6 +155,7 @@ struct fc_pool {
   int64_t prof_press_launches = 0, prof_total_launches = 0;
   bool prof_valid = false;
   int64_t last_paths[kNumPaths] = {0, 0, 0};  // press launches per path, last compress call
+  int last_prefill_tma = -1;                   // kernel of the last prefill write (-1: none yet)
   // host-resident compress (fc_pool_compress_host_batch): a copy stream, two
   // staging slots the DMA fills while the previous slot is scattered into
   // blocks, and a kept-index scratch for the zero-copy V gather.
@@ -973,7 +974,7 @@ fc_status fc_pool_write_prefill_kv(fc_pool* p, int32_t layer, int32_t n, const i
   if (n == 0) return FC_OK;
   DeviceGuard guard(p->device);
   return launch_write_prefill(p->g, p->arena, p->d_table, layer, n, reqs.data(), k, v,
-                              (cudaStream_t)stream);
+                              (cudaStream_t)stream, &p->last_prefill_tma);
 }
 
 fc_status fc_pool_decode_attention(fc_pool* p, int32_t layer, int32_t n, const int64_t* handle_ids,
@@ -1122,6 +1123,12 @@ fc_status fc_pool_last_profile(fc_pool* p, fc_profile* out) {
 fc_status fc_pool_last_paths(fc_pool* p, int64_t out[3]) {
   if (!p || !out) return set_error(FC_ERR_INVALID_ARG, "null argument");
   for (int k = 0; k < kNumPaths; ++k) out[k] = p->last_paths[k];
+  return FC_OK;
+}
+
+fc_status fc_pool_last_prefill_path(fc_pool* p, int32_t* tma) {
+  if (!p || !tma) return set_error(FC_ERR_INVALID_ARG, "null argument");
+  *tma = p->last_prefill_tma;
   return FC_OK;
 }
 

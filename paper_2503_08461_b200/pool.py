@@ -882,6 +882,14 @@ class KVCachePool:
         nv._check(nv.lib.fc_pool_last_paths(nv.ptr, out))
         return {"tc": int(out[0]), "simt": int(out[1]), "chunk": int(out[2])}
 
+    def last_prefill_path(self) -> str:
+        """Kernel of the most recent ``write_prefill_kv``: ``"tma"`` (TMA head-group tiles,
+        whole-chunk bulk stores), ``"copy"`` (register-copy kernel) or ``"none"``."""
+        nv = self._need_native()
+        out = ctypes.c_int32(-1)
+        nv._check(nv.lib.fc_pool_last_prefill_path(nv.ptr, ctypes.byref(out)))
+        return {1: "tma", 0: "copy"}.get(out.value, "none")
+
     def synchronize(self) -> None:
         if self._native is not None:
             self._native._check(self._native.lib.fc_pool_synchronize(self._native.ptr))

@@ -42,6 +42,7 @@ def test_prefill_write_then_knorm(cuda, dtype):
         k = torch.randn((sum(lens), 4, 128), generator=g, device=cuda).to(tdt)
         v = torch.randn((sum(lens), 4, 128), generator=g, device=cuda).to(tdt)
         pool.write_prefill_kv(hs, layer, k, v)
+        assert pool.last_prefill_path() == "tma"
         layers.append((k, v))
     dense = []
     off = 0
@@ -125,6 +126,8 @@ def test_prefill_geometries_and_ragged_chunks(cuda, H, D, bs, dtype):
                 beg.append(lo)
             pool.write_prefill_kv(hs, layer, torch.cat(ks).contiguous(), torch.cat(vs).contiguous(),
                                   seq_lens=seq, tok_begin=beg)
+            # the TMA ingest takes every chunk up to its 16-KB tile; bs 128 x 256 B is 32 KB
+            assert pool.last_prefill_path() == ("copy" if bs * D * bpe > 16384 else "tma")
     for i in range(n_req):
         got = pool.load_tokens(hs[i])                            # [L, 2, H, n, D]
         for layer in range(cfg.num_layers):
