@@ -11,9 +11,9 @@ from __future__ import annotations
 import ctypes
 import os
 
-LIB_PATH = os.environ.get(
-    "FASTCACHE_LIB",
-    os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libfastcache.so"))
+# FASTCACHE_LIB (non-empty) points at another build of the library, e.g. an A/B variant
+LIB_PATH = os.environ.get("FASTCACHE_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libfastcache.so")
 
 # fc_status
 OK = 0
