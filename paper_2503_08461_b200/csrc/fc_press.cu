@@ -500,6 +500,9 @@ __global__ void __launch_bounds__(kThreads, KIND == FC_PRESS_KNORM ? FC_KN_MINB 
 // row count, cast to the pool dtype (numpy mean semantics, kv.py:227-231);
 // SEEDED_LINEAR: fp64 weighted sum with the renormalised weights, rounded to
 // the pool dtype (the reference returns fp64; the pool stores its dtype).
+#ifndef FC_CHUNK_ITEMS   // output vectors per thread per chunk (c2m: 2 -> 4.69 ms, 4 -> 3.81, 8 spills)
+#define FC_CHUNK_ITEMS 4
+#endif
 #ifndef FC_CHUNK_MINB   // chunk-fold CTAs per SM the register budget is sized for
 #define FC_CHUNK_MINB 4
 #endif
@@ -510,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, kSeeded ? 2 : FC_CHUNK_MINB)
                       const __grid_constant__ PressBatch b, const PressParams pp) {
   constexpr int kVecs = D * (int)sizeof(T) / 16;
   constexpr int kEPV = RowCfg<T>::kEPV;
-  constexpr int kItems = 4;
+  constexpr int kItems = FC_CHUNK_ITEMS;   // output vectors per thread per chunk
   constexpr int kChunk = kThreads * kItems / (2 * kVecs);
   extern __shared__ __align__(16) unsigned char smem[];
   const int LH = g.L * g.H;
