@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, KIND == FC_PRESS_KNORM ? FC_KN_MINB 
 #ifndef FC_CHUNK_ITEMS   // output vectors per thread per chunk (c2m: 2 -> 4.69 ms, 4 -> 3.81, 8 spills)
 #define FC_CHUNK_ITEMS 4
 #endif
-#ifndef FC_CHUNK_MINB   // chunk-fold CTAs per SM the register budget is sized for
+#ifndef FC_CHUNK_MINB   // chunk-fold CTAs per SM the register budget is sized for (c2m: 3 -> 4.56 ms, 4 -> 3.81, 5 / 6 spill: 5.63 / 8.12)
 #define FC_CHUNK_MINB 4
 #endif
 template <typename T, int D, bool kSeeded>
